@@ -1,0 +1,173 @@
+/*
+ * treeattn_b200.h -- C ABI of the B200-native DeFT-Flatten decode path.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/treeattn, paths below relative to it).
+ * The reference is a header-only C++ library with no FFI of its own; the
+ * entry points here are exactly what a binding of its hot path needs:
+ *
+ *   reference call                                   | replaced by
+ *   -------------------------------------------------+---------------------------
+ *   DecodingTree(root_tokens, KvLifecycle*)  tree.hpp:40-51   | ta_tree_new
+ *   DecodingTree::restore(root, nodes, kv)   tree.hpp:207-238 | ta_tree_restore
+ *   DecodingTree::branch                     tree.hpp:74-97   | ta_tree_branch
+ *   DecodingTree::prune                      tree.hpp:100-116 | ta_tree_prune
+ *   DecodingTree::append_tokens              tree.hpp:119-129 | ta_tree_append
+ *   DecodingTree::leaves                     tree.hpp:55      | ta_tree_leaves
+ *   PagePool(dim, page_size) + KvLifecycle   kv_cache.hpp:33-147 | ta_ctx_create (device pool)
+ *   PagePool::page_count/free_page_count/live_slots kv_cache.hpp:43-45 | ta_pool_stats
+ *   KvHandle::refs[t] (TokenRef)             kv_cache.hpp:14-22 | ta_pool_token_ref
+ *   PagePool::write_kv                       kv_cache.hpp:104-116 | ta_kv_write
+ *   partition_flatten                        partition.hpp:212-253 | ta_plan_flatten
+ *   plan_to_json                             serde.hpp:41-61  | ta_plan_json
+ *   run_iteration(tree, Flatten, bs, pool, queries, params)
+ *                                            attention.hpp:293-334 | ta_prepare + ta_attend
+ *   io_measured / io_analytical(Flatten)     io_model.hpp:144-170 | ta_io_stats
+ *
+ * Errors: every entry returns a ta_status; ta_last_error() returns the
+ * thread-local message, mirroring the reference's exception text
+ * (invalid_argument / out_of_range / logic_error).  No exception crosses
+ * this boundary.  There is no CPU fallback: attention entry points on a
+ * context without a device fail with TA_ERR_NO_DEVICE.
+ */
+#ifndef TREEATTN_B200_H
+#define TREEATTN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TA_ABI_VERSION 1
+
+typedef int ta_status;
+enum {
+    TA_OK = 0,
+    TA_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    TA_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range */
+    TA_ERR_LOGIC = 3,            /* std::logic_error */
+    TA_ERR_CUDA = 4,
+    TA_ERR_NO_DEVICE = 5,
+    TA_ERR_OUT_OF_MEMORY = 6,
+};
+
+enum { TA_F32 = 0, TA_BF16 = 1 };
+
+typedef struct ta_shape {
+    int n_layers;        /* independent KV pools, one per layer */
+    int n_q_heads;       /* h_q of the model (AttentionParams::n_heads for MHA) */
+    int n_kv_heads;      /* h_kv (== n_q_heads for the reference's MHA) */
+    int d_head;          /* AttentionParams::d_head */
+    int kv_dtype;        /* TA_F32 | TA_BF16 : KV pool and query dtype */
+    int out_dtype;       /* TA_F32 | TA_BF16 : attention output dtype */
+    int page_tokens;     /* PagePool page_size (kv_cache.hpp:35), default 16 */
+    int kv_head_begin;   /* first kv head owned by this context (head sharding) */
+    int n_local_kv_heads;/* kv heads owned by this context (0 = all) */
+    int64_t max_pages;   /* device page capacity per (layer, kv head) pool */
+} ta_shape;
+
+typedef struct ta_ctx ta_ctx;
+
+const char* ta_last_error(void);
+int ta_abi_version(void);
+
+/* device < 0 creates a host-only context (tree, page accounting, planner). */
+ta_status ta_ctx_create(int device, const ta_shape* shape, ta_ctx** out);
+ta_status ta_ctx_destroy(ta_ctx* ctx);
+/* tuning knobs: "fma_max_rows", "use_mma", "span_tokens", "final_direct" */
+ta_status ta_set_option(ta_ctx* ctx, const char* key, int64_t value);
+
+/* ---- DecodingTree (tree mutations drive the page pool like KvLifecycle) -- */
+ta_status ta_tree_new(ta_ctx* ctx, int64_t root_tokens, int32_t* root_out);
+ta_status ta_tree_restore(ta_ctx* ctx, int32_t root, int n, const int32_t* ids,
+                          const int32_t* parents, const int64_t* token_counts);
+ta_status ta_tree_branch(ta_ctx* ctx, int32_t at, int n, const int64_t* child_token_counts,
+                         int32_t* created);
+ta_status ta_tree_prune(ta_ctx* ctx, int32_t at);
+ta_status ta_tree_append(ta_ctx* ctx, int32_t leaf, int64_t n);
+/* leaves in DFS pre-order; *n receives the count (out may be NULL to size) */
+ta_status ta_tree_leaves(ta_ctx* ctx, int32_t* out, int cap, int* n);
+
+typedef struct ta_tree_info {
+    int32_t root;
+    int32_t node_count;
+    int32_t n_leaves;
+    int32_t next_id;
+    int64_t total_tokens;
+    int64_t path_tokens_sum; /* sum of root-to-leaf path lengths (F_s numerator) */
+} ta_tree_info;
+ta_status ta_tree_get_info(ta_ctx* ctx, ta_tree_info* out);
+/* snapshot in ascending id order; *n receives node count */
+ta_status ta_tree_snapshot(ta_ctx* ctx, int32_t* ids, int32_t* parents, int64_t* counts,
+                           int cap, int* n);
+
+/* ---- PagePool accounting ------------------------------------------------ */
+ta_status ta_pool_stats(ta_ctx* ctx, int64_t* page_count, int64_t* free_pages,
+                        int64_t* live_slots);
+ta_status ta_pool_token_ref(ta_ctx* ctx, int32_t node, int64_t token, int32_t* page,
+                            int32_t* slot);
+
+/* ---- KV content ----------------------------------------------------------
+ * Rows [n_tok][n_local_kv_heads][d_head] in kv_dtype, for tokens
+ * [tok_begin, tok_begin+n_tok) of `node` in `layer`.  src_on_device selects
+ * device or host source pointers.  stream: cudaStream_t (NULL = default). */
+ta_status ta_kv_write(ta_ctx* ctx, int layer, int32_t node, int64_t tok_begin, int64_t n_tok,
+                      const void* k, const void* v, int src_on_device, void* stream);
+
+/* ---- Plan (bit-exact partition_flatten) ---------------------------------- */
+typedef struct ta_plan_view {
+    int block_size;
+    int n_groups;
+    const int32_t* seg_begin;   /* [n_groups+1] */
+    const int32_t* q_begin;     /* [n_groups+1] */
+    const int32_t* seg_node;    /* [n_segs] */
+    const int64_t* seg_offset;
+    const int64_t* seg_len;
+    const uint64_t* seg_mask;
+    const int32_t* queries;     /* leaf NodeIds */
+} ta_plan_view;
+/* arrays stay valid until the next plan call on this context */
+ta_status ta_plan_flatten(ta_ctx* ctx, int block_size, ta_plan_view* out);
+/* plan_to_json(partition_flatten(tree, bs)).dump(); *len excludes the NUL */
+ta_status ta_plan_json(ta_ctx* ctx, int block_size, char* buf, size_t cap, size_t* len);
+
+/* ---- Attention ------------------------------------------------------------
+ * ta_prepare: plan + device schedule + metadata upload for the current tree
+ * (once per decode step; reused by every layer).  ta_attend: one layer;
+ * q  [n_leaves][n_local_q_heads][d_head] in kv_dtype, leaves() order;
+ * out [n_leaves][n_local_q_heads][d_head] in out_dtype;
+ * lse (optional, may be NULL) [n_leaves][n_local_q_heads] fp32, natural log.
+ * Leaves whose path holds no tokens get lse = -inf and out = 0 (they are
+ * absent from the reference's AttentionOutput map). */
+ta_status ta_prepare(ta_ctx* ctx, int block_size, void* stream);
+ta_status ta_attend(ta_ctx* ctx, int layer, const void* q, void* out, float* lse, void* stream);
+/* End-to-end variant over HOST buffers (pinned or pageable): H2D q, attend,
+ * D2H out, synchronised on `stream` before returning. */
+ta_status ta_attend_host(ta_ctx* ctx, int layer, const void* q_host, void* out_host,
+                         void* stream);
+
+typedef struct ta_io_stats {
+    int64_t n_chunks;          /* flatten chunks (sibling groups fused) */
+    int64_t n_groups;          /* reference QkvGroups */
+    int64_t n_units;           /* CTA work units per kv head */
+    int64_t n_units_mma;
+    int64_t n_partials;        /* (unit, query) partial records per kv head */
+    int64_t kv_bytes;          /* unique KV bytes read per layer (this shard) */
+    int64_t kv_bytes_loaded;   /* KV bytes the schedule loads (incl. row-block re-reads) */
+    int64_t q_bytes;           /* query bytes per layer */
+    int64_t out_bytes;         /* output bytes per layer */
+    int64_t partial_bytes;     /* off-chip partial (m,l,O) bytes written+read per layer */
+    int64_t meta_bytes;        /* schedule metadata uploaded per step */
+    int64_t flops;             /* masked-in attention flops per layer (4*d per q-head-token) */
+} ta_io_stats;
+ta_status ta_io_stats_get(ta_ctx* ctx, ta_io_stats* out);
+
+/* number of kernels ta_attend launches per call (for launch accounting) */
+int ta_launches_per_attend(ta_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

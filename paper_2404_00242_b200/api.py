@@ -1,0 +1,230 @@
+"""Python mirror of the reference's operator API for the DeFT-Flatten path.
+
+The reference (/root/reference/proj/include/treeattn) is a C++ header
+library; its hot-path API is DecodingTree (tree.hpp) driving a PagePool
+through KvLifecycle (kv_cache.hpp), partition_flatten (partition.hpp) and
+run_iteration (attention.hpp:293).  ``TreeAttention`` bundles the three
+behind the C ABI: the tree and its page accounting live in the native
+context, the KV pages live in HBM, and attention runs on sm_100a kernels.
+Method names and error behaviour follow the reference (ValueError for
+std::invalid_argument, IndexError for std::out_of_range, RuntimeError for
+std::logic_error).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import capi
+from .capi import check, lib
+
+_DT = {"f32": capi.TA_F32, "float32": capi.TA_F32, "bf16": capi.TA_BF16, "bfloat16": capi.TA_BF16}
+
+
+def _ptr(x):
+    """Device/host pointer of a torch tensor or numpy array."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return C.c_void_p(x.data_ptr())
+    if isinstance(x, np.ndarray):
+        return C.c_void_p(x.ctypes.data)
+    return C.c_void_p(int(x))
+
+
+def _stream(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except ImportError:
+            pass
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+@dataclass
+class IoStats:
+    n_chunks: int
+    n_groups: int
+    n_units: int
+    n_units_mma: int
+    n_partials: int
+    kv_bytes: int
+    kv_bytes_loaded: int
+    q_bytes: int
+    out_bytes: int
+    partial_bytes: int
+    meta_bytes: int
+    flops: int
+
+
+class TreeAttention:
+    """Tree KV cache + DeFT-Flatten attention on one device (one head shard).
+
+    device=-1 gives a host-only context (tree, page accounting, planner)."""
+
+    def __init__(self, n_layers=1, n_q_heads=1, n_kv_heads=None, d_head=64, kv_dtype="f32",
+                 out_dtype="f32", page_tokens=16, max_pages=1 << 16, device=0, kv_head_begin=0,
+                 n_local_kv_heads=0):
+        n_kv_heads = n_q_heads if n_kv_heads is None else n_kv_heads
+        s = capi.Shape(n_layers, n_q_heads, n_kv_heads, d_head, _DT[kv_dtype], _DT[out_dtype],
+                       page_tokens, kv_head_begin, n_local_kv_heads, max_pages)
+        h = C.c_void_p()
+        check(lib().ta_ctx_create(device, C.byref(s), C.byref(h)), "ta_ctx_create")
+        self._h = h
+        self.n_layers, self.n_q_heads, self.n_kv_heads, self.d_head = n_layers, n_q_heads, n_kv_heads, d_head
+        self.kv_dtype, self.out_dtype = kv_dtype, out_dtype
+        self.page_tokens = page_tokens
+        self.device = device
+        self.n_local_kv_heads = n_local_kv_heads or (n_kv_heads - kv_head_begin)
+        self.kv_head_begin = kv_head_begin
+        self.group = n_q_heads // n_kv_heads
+        self.n_local_q_heads = self.n_local_kv_heads * self.group
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ta_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def set_option(self, key: str, value: int):
+        check(lib().ta_set_option(self._h, key.encode(), int(value)), "ta_set_option")
+
+    # ---------------------------------------------------------------- tree
+    def new_tree(self, root_tokens: int) -> int:
+        r = C.c_int32()
+        check(lib().ta_tree_new(self._h, int(root_tokens), C.byref(r)), "new_tree")
+        return r.value
+
+    def restore(self, root, ids, parents, counts):
+        ids = np.ascontiguousarray(ids, np.int32)
+        parents = np.ascontiguousarray(parents, np.int32)
+        counts = np.ascontiguousarray(counts, np.int64)
+        check(lib().ta_tree_restore(self._h, int(root), len(ids), ids.ctypes.data_as(C.POINTER(C.c_int32)),
+                                    parents.ctypes.data_as(C.POINTER(C.c_int32)),
+                                    counts.ctypes.data_as(C.POINTER(C.c_int64))), "restore")
+
+    def restore_snapshot(self, snap):
+        self.restore(*snap)
+
+    def branch(self, at: int, child_token_counts) -> list[int]:
+        cnt = np.ascontiguousarray(child_token_counts, np.int64)
+        out = np.zeros(len(cnt), np.int32)
+        check(lib().ta_tree_branch(self._h, int(at), len(cnt), cnt.ctypes.data_as(C.POINTER(C.c_int64)),
+                                   out.ctypes.data_as(C.POINTER(C.c_int32))), "branch")
+        return [int(x) for x in out]
+
+    def prune(self, at: int):
+        check(lib().ta_tree_prune(self._h, int(at)), "prune")
+
+    def append_tokens(self, leaf: int, n: int):
+        check(lib().ta_tree_append(self._h, int(leaf), int(n)), "append_tokens")
+
+    def leaves(self) -> np.ndarray:
+        n = C.c_int()
+        check(lib().ta_tree_leaves(self._h, None, 0, C.byref(n)), "leaves")
+        out = np.zeros(n.value, np.int32)
+        check(lib().ta_tree_leaves(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)), n.value, C.byref(n)),
+              "leaves")
+        return out
+
+    def info(self) -> dict:
+        i = capi.TreeInfo()
+        check(lib().ta_tree_get_info(self._h, C.byref(i)), "info")
+        return {f: getattr(i, f) for f, _ in capi.TreeInfo._fields_}
+
+    def snapshot(self):
+        n = C.c_int()
+        check(lib().ta_tree_snapshot(self._h, None, None, None, 0, C.byref(n)), "snapshot")
+        ids = np.zeros(n.value, np.int32)
+        par = np.zeros(n.value, np.int32)
+        cnt = np.zeros(n.value, np.int64)
+        check(lib().ta_tree_snapshot(self._h, ids.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     par.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     cnt.ctypes.data_as(C.POINTER(C.c_int64)), n.value, C.byref(n)), "snapshot")
+        return self.info()["root"], ids, par, cnt
+
+    # ---------------------------------------------------------------- pool
+    def pool_stats(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().ta_pool_stats(self._h, C.byref(a), C.byref(b), C.byref(c)), "pool_stats")
+        return {"page_count": a.value, "free_page_count": b.value, "live_slots": c.value}
+
+    def token_ref(self, node: int, token: int):
+        p, s = C.c_int32(), C.c_int32()
+        check(lib().ta_pool_token_ref(self._h, int(node), int(token), C.byref(p), C.byref(s)), "token_ref")
+        return p.value, s.value
+
+    def write_kv(self, layer: int, node: int, k, v, tok_begin: int = 0, stream=None):
+        """k, v: [n_tok][n_local_kv_heads][d_head] (torch device tensor or host numpy/torch)."""
+        n = int(k.shape[0])
+        on_dev = bool(getattr(k, "is_cuda", False))
+        check(lib().ta_kv_write(self._h, int(layer), int(node), int(tok_begin), n, _ptr(k), _ptr(v),
+                                int(on_dev), _stream(stream)), "write_kv")
+
+    # ---------------------------------------------------------------- plan
+    def plan_flatten(self, block_size: int = 128) -> dict:
+        """partition_flatten (partition.hpp:212-253) in oracle.core's plan format."""
+        pv = capi.PlanView()
+        check(lib().ta_plan_flatten(self._h, int(block_size), C.byref(pv)), "plan_flatten")
+        groups = []
+        for g in range(pv.n_groups):
+            s0, s1 = pv.seg_begin[g], pv.seg_begin[g + 1]
+            q0, q1 = pv.q_begin[g], pv.q_begin[g + 1]
+            groups.append({
+                "id": g,
+                "segments": [(pv.seg_node[s], pv.seg_offset[s], pv.seg_len[s]) for s in range(s0, s1)],
+                "queries": [pv.queries[q] for q in range(q0, q1)],
+                "masks": [pv.seg_mask[s] for s in range(s0, s1)],
+            })
+        return {"strategy": "flatten", "block_size": pv.block_size, "groups": groups}
+
+    def plan_json(self, block_size: int = 128) -> str:
+        n = C.c_size_t()
+        check(lib().ta_plan_json(self._h, int(block_size), None, 0, C.byref(n)), "plan_json")
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib().ta_plan_json(self._h, int(block_size), buf, n.value + 1, C.byref(n)), "plan_json")
+        return buf.value.decode()
+
+    # ----------------------------------------------------------- attention
+    def prepare(self, block_size: int = 128, stream=None):
+        check(lib().ta_prepare(self._h, int(block_size), _stream(stream)), "prepare")
+
+    def attend(self, layer: int, q, out=None, lse=None, stream=None):
+        """q [L][n_local_q_heads][d_head] device tensor -> out (same layout)."""
+        if out is None:
+            import torch
+            dt = torch.float32 if self.out_dtype in ("f32", "float32") else torch.bfloat16
+            out = torch.empty(q.shape, dtype=dt, device=q.device)
+        check(lib().ta_attend(self._h, int(layer), _ptr(q), _ptr(out), _ptr(lse), _stream(stream)), "attend")
+        return out
+
+    def attend_host(self, layer: int, q_host, out_host, stream=None):
+        check(lib().ta_attend_host(self._h, int(layer), _ptr(q_host), _ptr(out_host), _stream(stream)),
+              "attend_host")
+        return out_host
+
+    def io_stats(self) -> IoStats:
+        s = capi.IoStats()
+        check(lib().ta_io_stats_get(self._h, C.byref(s)), "io_stats")
+        return IoStats(**{f: getattr(s, f) for f, _ in capi.IoStats._fields_})
+
+    def launches_per_attend(self) -> int:
+        return lib().ta_launches_per_attend(self._h)
+
+
+def run_iteration(ctx: TreeAttention, layer: int, q, block_size: int = 128, lse=None, stream=None):
+    """run_iteration(tree, Strategy::Flatten, block_size, pool, queries, params)
+    (attention.hpp:293-334): plan + attention for one layer.  Returns
+    (out [L][h][d] device tensor, plan dict)."""
+    ctx.prepare(block_size, stream)
+    out = ctx.attend(layer, q, lse=lse, stream=stream)
+    return out, ctx.plan_flatten(block_size)

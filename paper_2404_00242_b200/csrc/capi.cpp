@@ -1,0 +1,577 @@
+// capi.cpp -- extern "C" boundary (include/treeattn_b200.h).  Owns the
+// context: tree mirror, page accounting, device KV pools, per-step schedule
+// metadata and scratch.  No exception crosses the boundary; there is no CPU
+// fallback for attention.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "ta_internal.h"
+#include "ta_kernels.h"
+#include "treeattn_b200.h"
+
+using namespace ta;
+
+struct ta_ctx {
+    int device = -1;
+    ta_shape shape{};
+    int G = 1;
+    int hq_loc = 1;
+    int esize = 4;
+    int out_esize = 4;
+    Tree tree;
+    PagePool pool;
+    Plan plan;
+    Schedule sched;
+    SchedOptions opt;
+    bool plan_valid = false;
+    uint64_t plan_version = ~0ull;
+    int plan_bs = -1;
+    bool prepared = false;
+    uint64_t prepared_version = ~0ull;
+    int prepared_bs = -1;
+
+    // device pools: one K and one V slab per layer, [n_loc][max_pages][P][D]
+    void* kv_k = nullptr;
+    void* kv_v = nullptr;
+    int64_t layer_elems = 0;  // elements per layer slab
+    int64_t head_stride = 0;  // elements per (layer, head) pool
+
+    // schedule metadata (one device blob) + pinned staging
+    void* meta_dev = nullptr;
+    size_t meta_cap = 0;
+    void* meta_host = nullptr;
+    size_t meta_host_cap = 0;
+    cudaEvent_t meta_done = nullptr;
+    const UnitDesc* d_units_fma = nullptr;
+    const UnitDesc* d_units_mma = nullptr;
+    const int32_t* d_tok_row = nullptr;
+    const uint32_t* d_tok_be = nullptr;
+    const int32_t* d_slot_leaf = nullptr;
+    const int32_t* d_slot_part = nullptr;
+    const int32_t* d_merge_leaf = nullptr;
+    const int32_t* d_merge_begin = nullptr;
+    const int32_t* d_merge_parts = nullptr;
+
+    // partial scratch
+    float* part = nullptr;
+    size_t part_cap = 0;  // floats
+
+    // staging for kv writes and host-buffer attend
+    void* stage_dev = nullptr;
+    size_t stage_cap = 0;
+    void* stage_host = nullptr;
+    size_t stage_host_cap = 0;
+    void* io_dev = nullptr;
+    size_t io_cap = 0;
+
+    ~ta_ctx() {
+        if (device >= 0) {
+            cudaSetDevice(device);
+            cudaFree(kv_k);
+            cudaFree(kv_v);
+            cudaFree(meta_dev);
+            cudaFreeHost(meta_host);
+            cudaFree(part);
+            cudaFree(stage_dev);
+            cudaFreeHost(stage_host);
+            cudaFree(io_dev);
+            if (meta_done) cudaEventDestroy(meta_done);
+        }
+    }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& m) {
+    g_err = m;
+    return code;
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return TA_OK;
+    } catch (const Error& e) {
+        return set_err(e.code, e.msg);
+    } catch (const std::bad_alloc&) {
+        return set_err(TA_ERR_OUT_OF_MEMORY, "host allocation failed");
+    } catch (const std::exception& e) {
+        return set_err(TA_ERR_LOGIC, e.what());
+    }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(e == cudaErrorMemoryAllocation ? TA_ERR_OUT_OF_MEMORY : TA_ERR_CUDA,
+             std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void need_device(const ta_ctx* c) {
+    if (c->device < 0) fail(TA_ERR_NO_DEVICE, "context has no CUDA device (host-only context)");
+}
+
+void grow_dev(void** p, size_t* cap, size_t need) {
+    if (need <= *cap) return;
+    size_t n = std::max(need, *cap * 2);
+    cudaFree(*p);
+    *p = nullptr;
+    cuda_check(cudaMalloc(p, n), "cudaMalloc");
+    *cap = n;
+}
+
+void grow_host(void** p, size_t* cap, size_t need) {
+    if (need <= *cap) return;
+    size_t n = std::max(need, *cap * 2);
+    cudaFreeHost(*p);
+    *p = nullptr;
+    cuda_check(cudaMallocHost(p, n), "cudaMallocHost");
+    *cap = n;
+}
+
+void ensure_plan(ta_ctx* c, int bs) {
+    if (c->plan_valid && c->plan_version == c->tree.version && c->plan_bs == bs) return;
+    plan_flatten(c->tree, bs, c->plan);
+    c->plan_valid = true;
+    c->plan_version = c->tree.version;
+    c->plan_bs = bs;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" {
+
+const char* ta_last_error(void) { return g_err.c_str(); }
+int ta_abi_version(void) { return TA_ABI_VERSION; }
+
+ta_status ta_ctx_create(int device, const ta_shape* s, ta_ctx** out) {
+    return guard([&] {
+        if (!s || !out) fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: null argument");
+        ta_shape sh = *s;
+        if (sh.page_tokens == 0) sh.page_tokens = 16;
+        if (sh.n_local_kv_heads == 0) sh.n_local_kv_heads = sh.n_kv_heads - sh.kv_head_begin;
+        if (sh.n_layers < 1 || sh.n_q_heads < 1 || sh.n_kv_heads < 1 || sh.d_head < 1 || sh.page_tokens < 1)
+            fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: dimensions must be positive");
+        if (sh.n_q_heads % sh.n_kv_heads != 0)
+            fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: n_q_heads must be a multiple of n_kv_heads");
+        if (sh.kv_head_begin < 0 || sh.n_local_kv_heads < 1 || sh.kv_head_begin + sh.n_local_kv_heads > sh.n_kv_heads)
+            fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: bad kv head shard");
+        if ((sh.kv_dtype != TA_F32 && sh.kv_dtype != TA_BF16) || (sh.out_dtype != TA_F32 && sh.out_dtype != TA_BF16))
+            fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: dtype must be TA_F32 or TA_BF16");
+        if (device >= 0 && sh.d_head != 16 && sh.d_head != 32 && sh.d_head != 64 && sh.d_head != 128)
+            fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: d_head must be 16, 32, 64 or 128 on the device");
+        auto c = std::make_unique<ta_ctx>();
+        c->shape = sh;
+        c->G = sh.n_q_heads / sh.n_kv_heads;
+        c->hq_loc = sh.n_local_kv_heads * c->G;
+        c->esize = sh.kv_dtype == TA_BF16 ? 2 : 4;
+        c->out_esize = sh.out_dtype == TA_BF16 ? 2 : 4;
+        c->pool.page_size = sh.page_tokens;
+        c->tree.hook = &c->pool;
+        if (device >= 0) {
+            int n = 0;
+            if (cudaGetDeviceCount(&n) != cudaSuccess || device >= n)
+                fail(TA_ERR_NO_DEVICE, "ta_ctx_create: CUDA device " + std::to_string(device) + " not available");
+            cuda_check(cudaSetDevice(device), "cudaSetDevice");
+            c->device = device;
+            if (sh.max_pages < 1) fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: max_pages must be >= 1");
+            c->pool.capacity = sh.max_pages;
+            c->head_stride = sh.max_pages * sh.page_tokens * (int64_t)sh.d_head;
+            c->layer_elems = c->head_stride * sh.n_local_kv_heads;
+            const size_t bytes = (size_t)c->layer_elems * sh.n_layers * c->esize;
+            cuda_check(cudaMalloc(&c->kv_k, bytes), "cudaMalloc(K pool)");
+            cuda_check(cudaMalloc(&c->kv_v, bytes), "cudaMalloc(V pool)");
+            cuda_check(cudaEventCreateWithFlags(&c->meta_done, cudaEventDisableTiming), "cudaEventCreate");
+            cudaDeviceProp prop;
+            cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+            c->opt.num_sms = prop.multiProcessorCount;
+        }
+        c->opt.use_mma = mma_supported(sh.d_head, sh.kv_dtype == TA_BF16);
+        *out = c.release();
+    });
+}
+
+ta_status ta_ctx_destroy(ta_ctx* c) {
+    delete c;
+    return TA_OK;
+}
+
+ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
+    return guard([&] {
+        const std::string k = key ? key : "";
+        if (k == "fma_max_rows") {
+            if (v < 1 || v > 16) fail(TA_ERR_INVALID_ARGUMENT, "fma_max_rows must be in [1, 16]");
+            c->opt.fma_max_rows = (int)v;
+        } else if (k == "use_mma") {
+            c->opt.use_mma = v != 0 && mma_supported(c->shape.d_head, c->shape.kv_dtype == TA_BF16);
+        } else if (k == "mma_max_rows") {
+            if (v != 64 && v != 128) fail(TA_ERR_INVALID_ARGUMENT, "mma_max_rows must be 64 or 128");
+            c->opt.mma_max_rows = (int)v;
+        } else if (k == "span_tokens") {
+            c->opt.span_tokens = (int)v;
+        } else if (k == "final_direct") {
+            c->opt.final_direct = v != 0;
+        } else if (k == "num_sms") {
+            c->opt.num_sms = (int)v;
+        } else {
+            fail(TA_ERR_INVALID_ARGUMENT, "unknown option " + k);
+        }
+        c->prepared = false;
+    });
+}
+
+// --------------------------------------------------------------------- tree
+ta_status ta_tree_new(ta_ctx* c, int64_t root_tokens, int32_t* root) {
+    return guard([&] {
+        if (root_tokens < 1) fail(TA_ERR_INVALID_ARGUMENT, "new_tree: root_token_count must be >= 1");
+        c->pool.reset();
+        c->tree.create(root_tokens);
+        if (root) *root = c->tree.root;
+    });
+}
+
+ta_status ta_tree_restore(ta_ctx* c, int32_t root, int n, const int32_t* ids, const int32_t* parents,
+                          const int64_t* counts) {
+    return guard([&] {
+        // validate on a scratch tree first so a bad snapshot leaves ctx intact
+        Tree probe;
+        probe.restore(root, n, ids, parents, counts);
+        c->pool.reset();
+        c->tree.restore(root, n, ids, parents, counts);
+    });
+}
+
+ta_status ta_tree_branch(ta_ctx* c, int32_t at, int n, const int64_t* counts, int32_t* created) {
+    return guard([&] {
+        auto ids = c->tree.branch(at, counts, n);
+        if (created) std::memcpy(created, ids.data(), ids.size() * sizeof(int32_t));
+    });
+}
+
+ta_status ta_tree_prune(ta_ctx* c, int32_t at) {
+    return guard([&] { c->tree.prune(at); });
+}
+
+ta_status ta_tree_append(ta_ctx* c, int32_t leaf, int64_t n) {
+    return guard([&] { c->tree.append(leaf, n); });
+}
+
+ta_status ta_tree_leaves(ta_ctx* c, int32_t* out, int cap, int* n) {
+    return guard([&] {
+        const int k = (int)c->tree.leaves.size();
+        if (n) *n = k;
+        if (out) std::memcpy(out, c->tree.leaves.data(), sizeof(int32_t) * std::min(k, cap));
+    });
+}
+
+ta_status ta_tree_get_info(ta_ctx* c, ta_tree_info* o) {
+    return guard([&] {
+        if (c->tree.root < 0) fail(TA_ERR_LOGIC, "no tree");
+        o->root = c->tree.root;
+        o->node_count = c->tree.n_alive;
+        o->n_leaves = (int32_t)c->tree.leaves.size();
+        o->next_id = c->tree.next_id;
+        o->total_tokens = c->tree.total_tokens();
+        int64_t p = 0;
+        for (int32_t l : c->tree.leaves) p += c->tree.path_tokens(l);
+        o->path_tokens_sum = p;
+    });
+}
+
+ta_status ta_tree_snapshot(ta_ctx* c, int32_t* ids, int32_t* parents, int64_t* counts, int cap, int* n) {
+    return guard([&] {
+        int k = 0;
+        for (int32_t id = 0; id < (int32_t)c->tree.alive.size(); ++id) {
+            if (!c->tree.alive[id]) continue;
+            if (ids && k < cap) {
+                ids[k] = id;
+                parents[k] = c->tree.parent[id];
+                counts[k] = c->tree.count[id];
+            }
+            ++k;
+        }
+        if (n) *n = k;
+    });
+}
+
+// --------------------------------------------------------------------- pool
+ta_status ta_pool_stats(ta_ctx* c, int64_t* page_count, int64_t* free_pages, int64_t* live_slots) {
+    return guard([&] {
+        if (page_count) *page_count = (int64_t)c->pool.pages.size();
+        if (free_pages) *free_pages = (int64_t)c->pool.free_list.size();
+        if (live_slots) *live_slots = c->pool.live_slots;
+    });
+}
+
+ta_status ta_pool_token_ref(ta_ctx* c, int32_t node, int64_t token, int32_t* page, int32_t* slot) {
+    return guard([&] {
+        const auto& h = c->pool.handle(node);
+        if (token < 0 || token >= h.n_tokens) fail(TA_ERR_INVALID_ARGUMENT, "token index out of range");
+        const int P = c->pool.page_size;
+        if (page) *page = h.pages[token / P];
+        if (slot) *slot = (int32_t)(token % P);
+    });
+}
+
+ta_status ta_kv_write(ta_ctx* c, int layer, int32_t node, int64_t t0, int64_t n, const void* k,
+                      const void* v, int src_on_device, void* stream) {
+    return guard([&] {
+        need_device(c);
+        if (layer < 0 || layer >= c->shape.n_layers) fail(TA_ERR_INVALID_ARGUMENT, "write_kv: layer out of range");
+        const auto& h = c->pool.handle(node);
+        if (t0 < 0 || n < 0 || t0 + n > h.n_tokens)
+            fail(TA_ERR_INVALID_ARGUMENT, "write_kv: token index out of range");
+        if (n == 0) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+        const int P = c->pool.page_size;
+        const int D = c->shape.d_head, nl = c->shape.n_local_kv_heads;
+        const size_t row_bytes = (size_t)nl * D * c->esize;
+        const size_t rows_bytes = align_up((size_t)n * 4, 256);
+        const size_t data_bytes = src_on_device ? 0 : align_up((size_t)n * row_bytes, 256);
+        grow_dev(&c->stage_dev, &c->stage_cap, rows_bytes + 2 * data_bytes);
+        grow_host(&c->stage_host, &c->stage_host_cap, rows_bytes);
+        int32_t* rows_h = (int32_t*)c->stage_host;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t tok = t0 + i;
+            rows_h[i] = (int32_t)(h.pages[tok / P] * P + tok % P);
+        }
+        char* base = (char*)c->stage_dev;
+        cuda_check(cudaMemcpyAsync(base, rows_h, n * 4, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(rows)");
+        const void* sk = k;
+        const void* sv = v;
+        if (!src_on_device) {
+            cuda_check(cudaMemcpyAsync(base + rows_bytes, k, n * row_bytes, cudaMemcpyHostToDevice, s), "H2D k");
+            cuda_check(cudaMemcpyAsync(base + rows_bytes + data_bytes, v, n * row_bytes, cudaMemcpyHostToDevice, s),
+                       "H2D v");
+            sk = base + rows_bytes;
+            sv = base + rows_bytes + data_bytes;
+        }
+        char* dk = (char*)c->kv_k + (size_t)layer * c->layer_elems * c->esize;
+        char* dv = (char*)c->kv_v + (size_t)layer * c->layer_elems * c->esize;
+        cuda_check(launch_kv_scatter(sk, sv, dk, dv, (const int32_t*)base, (int)n, nl, c->head_stride, D, c->esize, s),
+                   "kv_scatter");
+        // the pinned row list / device staging are reused by the next call
+        cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    });
+}
+
+// --------------------------------------------------------------------- plan
+ta_status ta_plan_flatten(ta_ctx* c, int bs, ta_plan_view* out) {
+    return guard([&] {
+        if (c->tree.root < 0) fail(TA_ERR_LOGIC, "no tree");
+        ensure_plan(c, bs);
+        const Plan& p = c->plan;
+        out->block_size = p.block_size;
+        out->n_groups = p.n_groups();
+        out->seg_begin = p.seg_begin.data();
+        out->q_begin = p.q_begin.data();
+        out->seg_node = p.seg_node.data();
+        out->seg_offset = p.seg_offset.data();
+        out->seg_len = p.seg_len.data();
+        out->seg_mask = p.seg_mask.data();
+        out->queries = p.queries.data();
+    });
+}
+
+ta_status ta_plan_json(ta_ctx* c, int bs, char* buf, size_t cap, size_t* len) {
+    return guard([&] {
+        if (c->tree.root < 0) fail(TA_ERR_LOGIC, "no tree");
+        ensure_plan(c, bs);
+        const std::string s = plan_json(c->tree, c->plan);
+        if (len) *len = s.size();
+        if (buf && cap) {
+            const size_t k = std::min(cap - 1, s.size());
+            std::memcpy(buf, s.data(), k);
+            buf[k] = 0;
+        }
+    });
+}
+
+// ---------------------------------------------------------------- attention
+ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
+    return guard([&] {
+        need_device(c);
+        if (c->tree.root < 0) fail(TA_ERR_LOGIC, "no tree");
+        cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+        // always re-plan: one decode step = plan + schedule + attention
+        plan_flatten(c->tree, bs, c->plan);
+        c->plan_valid = true;
+        c->plan_version = c->tree.version;
+        c->plan_bs = bs;
+        build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, c->shape.kv_dtype == TA_BF16,
+                       c->opt, c->sched);
+        const Schedule& S = c->sched;
+        if (c->opt.fma_max_rows > 16) fail(TA_ERR_INVALID_ARGUMENT, "fma_max_rows > 16");
+        // pack metadata into one blob
+        struct Part {
+            const void* src;
+            size_t bytes;
+            size_t off;
+        };
+        Part parts[9] = {
+            {S.units_fma.data(), S.units_fma.size() * sizeof(UnitDesc), 0},
+            {S.units_mma.data(), S.units_mma.size() * sizeof(UnitDesc), 0},
+            {S.tok_row.data(), S.tok_row.size() * 4, 0},
+            {S.tok_be.data(), S.tok_be.size() * 4, 0},
+            {S.slot_leaf.data(), S.slot_leaf.size() * 4, 0},
+            {S.slot_part.data(), S.slot_part.size() * 4, 0},
+            {S.merge_leaf.data(), S.merge_leaf.size() * 4, 0},
+            {S.merge_begin.data(), S.merge_begin.size() * 4, 0},
+            {S.merge_parts.data(), S.merge_parts.size() * 4, 0},
+        };
+        size_t total = 0;
+        for (auto& p : parts) {
+            p.off = total;
+            total = align_up(total + p.bytes, 256);
+        }
+        total = std::max<size_t>(total, 256);
+        // previous upload must have consumed the pinned staging
+        cuda_check(cudaEventSynchronize(c->meta_done), "cudaEventSynchronize");
+        grow_host(&c->meta_host, &c->meta_host_cap, total);
+        grow_dev(&c->meta_dev, &c->meta_cap, total);
+        for (auto& p : parts)
+            if (p.bytes) std::memcpy((char*)c->meta_host + p.off, p.src, p.bytes);
+        cudaStream_t s = (cudaStream_t)stream;
+        cuda_check(cudaMemcpyAsync(c->meta_dev, c->meta_host, total, cudaMemcpyHostToDevice, s), "metadata upload");
+        cuda_check(cudaEventRecord(c->meta_done, s), "cudaEventRecord");
+        char* d = (char*)c->meta_dev;
+        c->d_units_fma = (const UnitDesc*)(d + parts[0].off);
+        c->d_units_mma = (const UnitDesc*)(d + parts[1].off);
+        c->d_tok_row = (const int32_t*)(d + parts[2].off);
+        c->d_tok_be = (const uint32_t*)(d + parts[3].off);
+        c->d_slot_leaf = (const int32_t*)(d + parts[4].off);
+        c->d_slot_part = (const int32_t*)(d + parts[5].off);
+        c->d_merge_leaf = (const int32_t*)(d + parts[6].off);
+        c->d_merge_begin = (const int32_t*)(d + parts[7].off);
+        c->d_merge_parts = (const int32_t*)(d + parts[8].off);
+        // partial scratch: o [n_part][hq][D] + lse [n_part][hq]
+        const size_t pf = (size_t)std::max(1, S.n_partials) * c->hq_loc * (c->shape.d_head + 1);
+        if (pf > c->part_cap) {
+            void* p = c->part;
+            size_t cap = c->part_cap * sizeof(float);
+            grow_dev(&p, &cap, pf * sizeof(float));
+            c->part = (float*)p;
+            c->part_cap = cap / sizeof(float);
+        }
+        c->prepared = true;
+        c->prepared_version = c->tree.version;
+        c->prepared_bs = bs;
+    });
+}
+
+static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* lse, cudaStream_t s) {
+    if (!c->prepared || c->prepared_version != c->tree.version)
+        fail(TA_ERR_LOGIC, "ta_attend: tree changed since ta_prepare (call ta_prepare first)");
+    if (layer < 0 || layer >= c->shape.n_layers) fail(TA_ERR_INVALID_ARGUMENT, "attend: layer out of range");
+    const Schedule& S = c->sched;
+    const int D = c->shape.d_head;
+    AttnArgs a{};
+    a.k = (const char*)c->kv_k + (size_t)layer * c->layer_elems * c->esize;
+    a.v = (const char*)c->kv_v + (size_t)layer * c->layer_elems * c->esize;
+    a.head_stride = c->head_stride;
+    a.q = q;
+    a.out = out;
+    a.lse = lse;
+    a.part_o = c->part;
+    a.part_lse = c->part + (size_t)std::max(1, S.n_partials) * c->hq_loc * D;
+    a.tok_row = c->d_tok_row;
+    a.tok_be = c->d_tok_be;
+    a.slot_leaf = c->d_slot_leaf;
+    a.slot_part = c->d_slot_part;
+    a.G = c->G;
+    a.hq_loc = c->hq_loc;
+    a.n_kv_loc = c->shape.n_local_kv_heads;
+    a.D = D;
+    a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+    a.kv_bf16 = c->shape.kv_dtype == TA_BF16;
+    a.out_bf16 = c->shape.out_dtype == TA_BF16;
+    if (!S.units_fma.empty()) {
+        a.units = c->d_units_fma;
+        a.n_units = (int)S.units_fma.size();
+        cuda_check(launch_attn_fma(a, c->opt.fma_max_rows, s), "attn_fma");
+    }
+    if (!S.units_mma.empty()) {
+        a.units = c->d_units_mma;
+        a.n_units = (int)S.units_mma.size();
+        cuda_check(launch_attn_mma(a, s), "attn_mma");
+    }
+    MergeArgs m{};
+    m.part_o = a.part_o;
+    m.part_lse = a.part_lse;
+    m.merge_leaf = c->d_merge_leaf;
+    m.merge_begin = c->d_merge_begin;
+    m.merge_parts = c->d_merge_parts;
+    m.n_merge = (int)S.merge_leaf.size();
+    m.out = out;
+    m.lse = lse;
+    m.hq_loc = c->hq_loc;
+    m.D = D;
+    m.out_bf16 = a.out_bf16;
+    cuda_check(launch_merge(m, s), "merge");
+}
+
+ta_status ta_attend(ta_ctx* c, int layer, const void* q, void* out, float* lse, void* stream) {
+    return guard([&] {
+        need_device(c);
+        attend_impl(c, layer, q, out, lse, (cudaStream_t)stream);
+    });
+}
+
+ta_status ta_attend_host(ta_ctx* c, int layer, const void* q_host, void* out_host, void* stream) {
+    return guard([&] {
+        need_device(c);
+        cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+        cudaStream_t s = (cudaStream_t)stream;
+        const size_t L = c->tree.leaves.size();
+        const size_t qb = L * c->hq_loc * c->shape.d_head * c->esize;
+        const size_t ob = L * c->hq_loc * c->shape.d_head * c->out_esize;
+        grow_dev(&c->io_dev, &c->io_cap, align_up(qb, 256) + ob);
+        char* dq = (char*)c->io_dev;
+        char* dout = dq + align_up(qb, 256);
+        cuda_check(cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, s), "H2D q");
+        attend_impl(c, layer, dq, dout, nullptr, s);
+        cuda_check(cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, s), "D2H out");
+        cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    });
+}
+
+ta_status ta_io_stats_get(ta_ctx* c, ta_io_stats* o) {
+    return guard([&] {
+        if (!c->prepared) fail(TA_ERR_LOGIC, "ta_io_stats: call ta_prepare first");
+        const Schedule& S = c->sched;
+        const int64_t D = c->shape.d_head, nl = c->shape.n_local_kv_heads;
+        const int64_t L = (int64_t)c->tree.leaves.size();
+        std::memset(o, 0, sizeof(*o));
+        o->n_chunks = c->plan.n_chunks();
+        o->n_groups = c->plan.n_groups();
+        o->n_units = (int64_t)(S.units_fma.size() + S.units_mma.size());
+        o->n_units_mma = (int64_t)S.units_mma.size();
+        o->n_partials = S.n_partials;
+        o->kv_bytes = S.kv_tokens_unique * 2 * nl * D * c->esize;
+        o->kv_bytes_loaded = S.kv_tokens_loaded * 2 * nl * D * c->esize;
+        o->q_bytes = L * c->hq_loc * D * c->esize;
+        o->out_bytes = L * c->hq_loc * D * c->out_esize;
+        o->partial_bytes = (int64_t)S.n_partials * c->hq_loc * (D + 1) * 4 * 2;
+        o->meta_bytes = (int64_t)(S.units_fma.size() + S.units_mma.size()) * sizeof(UnitDesc) +
+                        (int64_t)(S.tok_row.size() + S.tok_be.size() + S.slot_leaf.size() + S.slot_part.size() +
+                                  S.merge_leaf.size() + S.merge_begin.size() + S.merge_parts.size()) * 4;
+        o->flops = S.masked_q_tokens * c->hq_loc * 4 * D;
+    });
+}
+
+int ta_launches_per_attend(ta_ctx* c) {
+    if (!c || !c->prepared) return 0;
+    return (c->sched.units_fma.empty() ? 0 : 1) + (c->sched.units_mma.empty() ? 0 : 1) +
+           (c->sched.merge_leaf.empty() ? 0 : 1);
+}
+
+}  // extern "C"

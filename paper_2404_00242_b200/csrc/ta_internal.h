@@ -1,0 +1,166 @@
+// ta_internal.h -- host-side data structures of the B200 DeFT-Flatten path.
+//
+// Tree / page pool / planner mirror the reference semantics (citations are
+// relative to /root/reference/proj/include/treeattn); the device schedule and
+// kernels are this framework's own design.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace ta {
+
+// ---------------------------------------------------------------------------
+// Errors: mapped 1:1 to the reference's exception classes at the C boundary.
+struct Error : std::exception {
+    int code;
+    std::string msg;
+    Error(int c, std::string m) : code(c), msg(std::move(m)) {}
+    const char* what() const noexcept override { return msg.c_str(); }
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+
+// ---------------------------------------------------------------------------
+// DecodingTree (tree.hpp:38-269): ids sequential and never reused; children in
+// insertion order (ascending id after restore); leaves() in DFS pre-order.
+// Flat arrays indexed by node id plus derived DFS data rebuilt per mutation.
+class KvHook {
+public:
+    virtual ~KvHook() = default;
+    virtual void on_alloc(int32_t node, int64_t n) = 0;   // KvLifecycle (tree.hpp:19-25)
+    virtual void on_extend(int32_t node, int64_t n) = 0;
+    virtual void on_free(int32_t node) = 0;
+};
+
+struct Tree {
+    int32_t root = -1;
+    int32_t next_id = 0;
+    int32_t n_alive = 0;
+    std::vector<uint8_t> alive;
+    std::vector<int32_t> parent;
+    std::vector<int64_t> count;
+    std::vector<std::vector<int32_t>> kids;
+    KvHook* hook = nullptr;
+
+    // derived (rebuild())
+    std::vector<int32_t> dfs;      // pre-order
+    std::vector<int32_t> leaves;   // leaf ids, DFS order
+    std::vector<int32_t> leaf_lo;  // per id: [lo, hi) range of leaf indices under it
+    std::vector<int32_t> leaf_hi;
+    uint64_t version = 0;
+
+    bool contains(int32_t id) const { return id >= 0 && id < (int32_t)alive.size() && alive[id]; }
+    void reserve(int32_t n);
+    void rebuild();
+    void create(int64_t root_tokens);                                   // tree.hpp:40-51
+    void restore(int32_t root, int n, const int32_t* ids, const int32_t* parents,
+                 const int64_t* counts);                                // tree.hpp:207-238
+    std::vector<int32_t> branch(int32_t at, const int64_t* counts, int n);   // tree.hpp:74-97
+    void prune(int32_t at);                                             // tree.hpp:100-116
+    void append(int32_t leaf, int64_t n);                               // tree.hpp:119-129
+    int64_t total_tokens() const;
+    int64_t path_tokens(int32_t leaf) const;
+    void subtree(int32_t at, std::vector<int32_t>& out) const;
+};
+
+// ---------------------------------------------------------------------------
+// PagePool accounting (kv_cache.hpp:33-187): page-per-node ownership, tail
+// fill, LIFO free list.  Token t of a node lives at pages[t / P], slot t % P.
+struct PagePool : KvHook {
+    int page_size = 16;
+    int64_t capacity = -1;  // device page capacity (-1: unbounded, host-only)
+    struct Page {
+        int32_t owner = -1;
+        int32_t used = 0;
+        int32_t live = 0;
+    };
+    struct Handle {
+        std::vector<int32_t> pages;
+        int64_t n_tokens = 0;
+    };
+    std::vector<Page> pages;
+    std::vector<int32_t> free_list;
+    std::unordered_map<int32_t, Handle> handles;
+    int64_t live_slots = 0;
+
+    void allocate(int32_t node, int64_t n);   // kv_cache.hpp:56-66
+    void extend(int32_t node, int64_t n);     // kv_cache.hpp:68-89
+    void release(int32_t node);               // kv_cache.hpp:91-102
+    int32_t acquire_page(int32_t owner);      // kv_cache.hpp:158-173
+    const Handle& handle(int32_t node) const;
+    void reset();
+    void on_alloc(int32_t node, int64_t n) override { allocate(node, n); }
+    void on_extend(int32_t node, int64_t n) override { extend(node, n); }
+    void on_free(int32_t node) override { release(node); }
+};
+
+// ---------------------------------------------------------------------------
+// Reference plan (partition.hpp:37-68) plus the fused chunk view the device
+// schedule is built from.
+struct Plan {
+    int block_size = 128;
+    // QkvGroups exactly as partition_flatten emits them
+    std::vector<int32_t> seg_begin{0}, q_begin{0};
+    std::vector<int32_t> seg_node, queries;
+    std::vector<int64_t> seg_offset, seg_len;
+    std::vector<uint64_t> seg_mask;
+    // chunks = one per flush (sibling groups of a >64-query split fused)
+    std::vector<int32_t> chunk_seg_begin{0};   // into cseg_*
+    std::vector<int32_t> chunk_q_begin{0};     // into chunk_q
+    std::vector<int32_t> cseg_node;
+    std::vector<int64_t> cseg_offset, cseg_len;
+    std::vector<int32_t> cseg_lo, cseg_hi;     // attending leaf-index interval
+    std::vector<int32_t> chunk_q;              // sorted leaf indices
+    int n_groups() const { return (int)seg_begin.size() - 1; }
+    int n_chunks() const { return (int)chunk_seg_begin.size() - 1; }
+};
+
+void plan_flatten(const Tree& t, int block_size, Plan& out);   // partition.hpp:212-253
+std::string plan_json(const Tree& t, const Plan& p);           // serde.hpp:41-61
+
+// ---------------------------------------------------------------------------
+// Device schedule (this framework's layout).
+// A unit is one CTA's work for one kv head: a span of consecutive chunks and
+// a block of query slots (local slot j <-> leaf index unit_slot[slot_begin+j]).
+// Its tokens are listed in stream order; per token the row index inside a
+// (layer, head) slab (page * P + slot) and the local slot range [b, e) whose
+// queries attend it.
+struct UnitDesc {
+    int32_t tok_begin;   // into tok_row / tok_be
+    int32_t n_tokens;
+    int32_t slot_begin;  // into slot_leaf / slot_part
+    int32_t n_slots;
+};
+
+struct Schedule {
+    std::vector<UnitDesc> units_fma, units_mma;
+    std::vector<int32_t> tok_row;     // page * P + slot
+    std::vector<uint32_t> tok_be;     // b | e << 16
+    std::vector<int32_t> slot_leaf;   // leaf index
+    std::vector<int32_t> slot_part;   // partial id, or -1 - leaf for direct final write
+    std::vector<int32_t> merge_leaf;  // leaves merged by the merge kernel
+    std::vector<int32_t> merge_begin; // [n_merge+1] into merge_parts
+    std::vector<int32_t> merge_parts; // partial ids in deterministic order
+    int32_t n_partials = 0;
+    int32_t n_leaves = 0;
+    int64_t kv_tokens_unique = 0;
+    int64_t kv_tokens_loaded = 0;
+    int64_t masked_q_tokens = 0;      // sum over leaves of path tokens (flops / (4 d h_q))
+};
+
+struct SchedOptions {
+    int fma_max_rows = 8;      // rows (= slots * G) above which a chunk goes to MMA
+    int mma_max_rows = 128;    // rows per MMA unit (one TMEM row tile)
+    bool use_mma = true;       // bf16 only
+    int span_tokens = 0;       // 0 = auto
+    bool final_direct = true;  // single-partial leaves written directly
+    int num_sms = 148;
+};
+
+void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int group_size,
+                    int n_kv_heads_local, bool bf16, const SchedOptions& opt, Schedule& out);
+
+}  // namespace ta
