@@ -164,6 +164,29 @@ typedef struct ta_io_stats {
 } ta_io_stats;
 ta_status ta_io_stats_get(ta_ctx* ctx, ta_io_stats* out);
 
+/* Device schedule of the current tree (built on the host; works on host-only
+ * contexts).  Unit u of kind k (0 = FMA, 1 = MMA) covers tokens
+ * [tok_begin, tok_begin+n_tokens) of tok_row/tok_be and slots
+ * [slot_begin, slot_begin+n_slots) of slot_leaf/slot_part.  tok_row =
+ * page * page_tokens + slot; tok_be = b | e << 16: local slots [b, e) attend.
+ * slot_part >= 0: partial id merged in merge order; < 0: -1-leaf, written
+ * directly.  Arrays stay valid until the next schedule/prepare call. */
+typedef struct ta_schedule_view {
+    int32_t n_units;
+    const int32_t* unit_kind;
+    const int32_t* unit_desc;   /* [n_units][4]: tok_begin, n_tokens, slot_begin, n_slots */
+    const int32_t* tok_row;
+    const uint32_t* tok_be;
+    const int32_t* slot_leaf;   /* leaf index in leaves() order */
+    const int32_t* slot_part;
+    int32_t n_merge;
+    const int32_t* merge_leaf;
+    const int32_t* merge_begin; /* [n_merge+1] */
+    const int32_t* merge_parts;
+    int32_t n_partials;
+} ta_schedule_view;
+ta_status ta_schedule_get(ta_ctx* ctx, int block_size, ta_schedule_view* out);
+
 /* number of kernels ta_attend launches per call (for launch accounting) */
 int ta_launches_per_attend(ta_ctx* ctx);
 

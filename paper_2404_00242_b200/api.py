@@ -217,6 +217,24 @@ class TreeAttention:
         check(lib().ta_io_stats_get(self._h, C.byref(s)), "io_stats")
         return IoStats(**{f: getattr(s, f) for f, _ in capi.IoStats._fields_})
 
+    def schedule(self, block_size: int = 128) -> dict:
+        """The device schedule (units, per-token rows/masks, merge lists) as numpy arrays."""
+        v = capi.ScheduleView()
+        check(lib().ta_schedule_get(self._h, int(block_size), C.byref(v)), "schedule")
+
+        def arr(p, n, dt):
+            return np.ctypeslib.as_array(p, shape=(n,)).astype(dt) if n else np.zeros(0, dt)
+        desc = arr(v.unit_desc, 4 * v.n_units, np.int64).reshape(-1, 4)
+        n_tok = int(desc[:, 0].max() + desc[desc[:, 0].argmax(), 1]) if v.n_units else 0
+        n_slot = int((desc[:, 2] + desc[:, 3]).max()) if v.n_units else 0
+        n_mp = v.merge_begin[v.n_merge] if v.n_merge else 0
+        return {"kind": arr(v.unit_kind, v.n_units, np.int64), "desc": desc,
+                "tok_row": arr(v.tok_row, n_tok, np.int64), "tok_be": arr(v.tok_be, n_tok, np.int64),
+                "slot_leaf": arr(v.slot_leaf, n_slot, np.int64), "slot_part": arr(v.slot_part, n_slot, np.int64),
+                "merge_leaf": arr(v.merge_leaf, v.n_merge, np.int64),
+                "merge_begin": arr(v.merge_begin, v.n_merge + 1, np.int64),
+                "merge_parts": arr(v.merge_parts, n_mp, np.int64), "n_partials": v.n_partials}
+
     def launches_per_attend(self) -> int:
         return lib().ta_launches_per_attend(self._h)
 

@@ -27,7 +27,7 @@ EXPORTED = [
     "ta_tree_new", "ta_tree_restore", "ta_tree_branch", "ta_tree_prune", "ta_tree_append",
     "ta_tree_leaves", "ta_tree_get_info", "ta_tree_snapshot", "ta_pool_stats", "ta_pool_token_ref",
     "ta_kv_write", "ta_plan_flatten", "ta_plan_json", "ta_prepare", "ta_attend", "ta_attend_host",
-    "ta_io_stats_get", "ta_launches_per_attend",
+    "ta_io_stats_get", "ta_launches_per_attend", "ta_schedule_get",
 ]
 
 
@@ -88,6 +88,15 @@ class IoStats(C.Structure):
         "q_bytes", "out_bytes", "partial_bytes", "meta_bytes", "flops")]
 
 
+class ScheduleView(C.Structure):
+    _fields_ = [("n_units", C.c_int32), ("unit_kind", C.POINTER(C.c_int32)), ("unit_desc", C.POINTER(C.c_int32)),
+                ("tok_row", C.POINTER(C.c_int32)), ("tok_be", C.POINTER(C.c_uint32)),
+                ("slot_leaf", C.POINTER(C.c_int32)), ("slot_part", C.POINTER(C.c_int32)),
+                ("n_merge", C.c_int32), ("merge_leaf", C.POINTER(C.c_int32)),
+                ("merge_begin", C.POINTER(C.c_int32)), ("merge_parts", C.POINTER(C.c_int32)),
+                ("n_partials", C.c_int32)]
+
+
 _lib = None
 
 
@@ -126,6 +135,7 @@ def lib():
         "ta_attend_host": (C.c_int, [vp, C.c_int, vp, vp, vp]),
         "ta_io_stats_get": (C.c_int, [vp, C.POINTER(IoStats)]),
         "ta_launches_per_attend": (C.c_int, [vp]),
+        "ta_schedule_get": (C.c_int, [vp, C.c_int, C.POINTER(ScheduleView)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -34,6 +34,11 @@ struct ta_ctx {
     uint64_t prepared_version = ~0ull;
     int prepared_bs = -1;
 
+    // TMA descriptors (CUtensorMap, 128 B) over the whole K / V pools
+    alignas(64) unsigned char tmap_k[128];
+    alignas(64) unsigned char tmap_v[128];
+    bool tmaps_ok = false;
+
     // device pools: one K and one V slab per layer, [n_loc][max_pages][P][D]
     void* kv_k = nullptr;
     void* kv_v = nullptr;
@@ -55,6 +60,12 @@ struct ta_ctx {
     const int32_t* d_merge_leaf = nullptr;
     const int32_t* d_merge_begin = nullptr;
     const int32_t* d_merge_parts = nullptr;
+    const int32_t* d_grp_row = nullptr;
+    const uint32_t* d_grp_info = nullptr;
+
+    // host copy of the schedule for ta_schedule_get
+    Schedule dbg_sched;
+    std::vector<int32_t> dbg_kind, dbg_desc;
 
     // partial scratch
     float* part = nullptr;
@@ -193,6 +204,12 @@ ta_status ta_ctx_create(int device, const ta_shape* s, ta_ctx** out) {
             cudaDeviceProp prop;
             cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
             c->opt.num_sms = prop.multiProcessorCount;
+            if (mma_supported(sh.d_head, sh.kv_dtype == TA_BF16)) {
+                const int64_t rows = (int64_t)sh.n_layers * sh.n_local_kv_heads * sh.max_pages * sh.page_tokens;
+                c->tmaps_ok = make_pool_tmap(c->tmap_k, c->kv_k, rows, sh.d_head) &&
+                              make_pool_tmap(c->tmap_v, c->kv_v, rows, sh.d_head);
+                if (!c->tmaps_ok) fail(TA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the KV pools");
+            }
         }
         c->opt.use_mma = mma_supported(sh.d_head, sh.kv_dtype == TA_BF16);
         *out = c.release();
@@ -417,7 +434,7 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             size_t bytes;
             size_t off;
         };
-        Part parts[9] = {
+        Part parts[11] = {
             {S.units_fma.data(), S.units_fma.size() * sizeof(UnitDesc), 0},
             {S.units_mma.data(), S.units_mma.size() * sizeof(UnitDesc), 0},
             {S.tok_row.data(), S.tok_row.size() * 4, 0},
@@ -427,6 +444,8 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             {S.merge_leaf.data(), S.merge_leaf.size() * 4, 0},
             {S.merge_begin.data(), S.merge_begin.size() * 4, 0},
             {S.merge_parts.data(), S.merge_parts.size() * 4, 0},
+            {S.grp_row.data(), S.grp_row.size() * 4, 0},
+            {S.grp_info.data(), S.grp_info.size() * 4, 0},
         };
         size_t total = 0;
         for (auto& p : parts) {
@@ -453,6 +472,8 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         c->d_merge_leaf = (const int32_t*)(d + parts[6].off);
         c->d_merge_begin = (const int32_t*)(d + parts[7].off);
         c->d_merge_parts = (const int32_t*)(d + parts[8].off);
+        c->d_grp_row = (const int32_t*)(d + parts[9].off);
+        c->d_grp_info = (const uint32_t*)(d + parts[10].off);
         // partial scratch: o [n_part][hq][D] + lse [n_part][hq]
         const size_t pf = (size_t)std::max(1, S.n_partials) * c->hq_loc * (c->shape.d_head + 1);
         if (pf > c->part_cap) {
@@ -494,6 +515,12 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     a.kv_bf16 = c->shape.kv_dtype == TA_BF16;
     a.out_bf16 = c->shape.out_dtype == TA_BF16;
+    a.tmap_k = c->tmap_k;
+    a.tmap_v = c->tmap_v;
+    a.head_rows = c->shape.max_pages * c->shape.page_tokens;
+    a.layer_row0 = (int64_t)layer * c->shape.n_local_kv_heads * a.head_rows;
+    a.grp_row = c->d_grp_row;
+    a.grp_info = c->d_grp_info;
     if (!S.units_fma.empty()) {
         a.units = c->d_units_fma;
         a.n_units = (int)S.units_fma.size();
@@ -563,8 +590,38 @@ ta_status ta_io_stats_get(ta_ctx* c, ta_io_stats* o) {
         o->partial_bytes = (int64_t)S.n_partials * c->hq_loc * (D + 1) * 4 * 2;
         o->meta_bytes = (int64_t)(S.units_fma.size() + S.units_mma.size()) * sizeof(UnitDesc) +
                         (int64_t)(S.tok_row.size() + S.tok_be.size() + S.slot_leaf.size() + S.slot_part.size() +
-                                  S.merge_leaf.size() + S.merge_begin.size() + S.merge_parts.size()) * 4;
+                                  S.merge_leaf.size() + S.merge_begin.size() + S.merge_parts.size() +
+                                  S.grp_row.size() + S.grp_info.size()) * 4;
         o->flops = S.masked_q_tokens * c->hq_loc * 4 * D;
+    });
+}
+
+ta_status ta_schedule_get(ta_ctx* c, int bs, ta_schedule_view* o) {
+    return guard([&] {
+        if (c->tree.root < 0) fail(TA_ERR_LOGIC, "no tree");
+        ensure_plan(c, bs);
+        Schedule& S = c->dbg_sched;
+        build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, c->shape.kv_dtype == TA_BF16,
+                       c->opt, S);
+        c->dbg_kind.clear();
+        c->dbg_desc.clear();
+        for (int k = 0; k < 2; ++k)
+            for (const UnitDesc& u : k ? S.units_mma : S.units_fma) {
+                c->dbg_kind.push_back(k);
+                c->dbg_desc.insert(c->dbg_desc.end(), {u.tok_begin, u.n_tokens, u.slot_begin, u.n_slots});
+            }
+        o->n_units = (int32_t)c->dbg_kind.size();
+        o->unit_kind = c->dbg_kind.data();
+        o->unit_desc = c->dbg_desc.data();
+        o->tok_row = S.tok_row.data();
+        o->tok_be = S.tok_be.data();
+        o->slot_leaf = S.slot_leaf.data();
+        o->slot_part = S.slot_part.data();
+        o->n_merge = (int32_t)S.merge_leaf.size();
+        o->merge_leaf = S.merge_leaf.data();
+        o->merge_begin = S.merge_begin.data();
+        o->merge_parts = S.merge_parts.data();
+        o->n_partials = S.n_partials;
     });
 }
 

@@ -533,8 +533,10 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                 // the segment's interval must intersect the block itself
                 const int32_t* lo_it = std::lower_bound(bq, bq + nb, plan.cseg_lo[s]);
                 if (lo_it == bq + nb || *lo_it >= plan.cseg_hi[s]) continue;
+                // attended only by this chunk's block: the unit may hold other
+                // slots (from neighbouring chunks) that belong to a sibling block here
                 u.pieces.push_back({plan.cseg_node[s], plan.cseg_offset[s], plan.cseg_len[s],
-                                    plan.cseg_lo[s], plan.cseg_hi[s]});
+                                    std::max(plan.cseg_lo[s], bq[0]), std::min(plan.cseg_hi[s], bq[nb - 1] + 1)});
                 u.tokens += plan.cseg_len[s];
             }
         u.last_chunk = bl.chunk;
@@ -573,6 +575,24 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
         }
         d.n_tokens = (int32_t)(S.tok_row.size() - d.tok_begin);
         S.kv_tokens_loaded += d.n_tokens;
+        d.grp_begin = (int32_t)S.grp_row.size();
+        d.n_grp = 0;
+        d.pad0 = d.pad1 = 0;
+        if (u.mma) {
+            for (int32_t k = d.tok_begin; k < d.tok_begin + d.n_tokens;) {
+                const int32_t row0 = S.tok_row[k];
+                const uint32_t be = S.tok_be[k];
+                int cnt = 1;
+                while (cnt < 16 && k + cnt < d.tok_begin + d.n_tokens && S.tok_row[k + cnt] == row0 + cnt &&
+                       S.tok_be[k + cnt] == be)
+                    ++cnt;
+                S.grp_row.push_back(row0);
+                S.grp_info.push_back(grp_pack(cnt, (int)(be & 0xffffu), (int)(be >> 16)));
+                k += cnt;
+            }
+            d.n_grp = (int32_t)S.grp_row.size() - d.grp_begin;
+            S.kv_tokens_loaded += 16LL * d.n_grp - d.n_tokens;  // box over-read
+        }
         dst.push_back(d);
     };
     for (const auto& u : done) emit(u, u.mma ? S.units_mma : S.units_fma);

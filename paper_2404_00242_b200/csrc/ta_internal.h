@@ -133,12 +133,24 @@ struct UnitDesc {
     int32_t n_tokens;
     int32_t slot_begin;  // into slot_leaf / slot_part
     int32_t n_slots;
+    int32_t grp_begin;   // MMA units: into grp_row / grp_info
+    int32_t n_grp;
+    int32_t pad0, pad1;
 };
+
+// MMA units load KV as TMA boxes of 16 consecutive pool rows ("groups"):
+// a group is a run of <= 16 tokens with consecutive rows and one attending
+// slot range; rows of the box past `count` are masked.
+inline uint32_t grp_pack(int count, int b, int e) {
+    return (uint32_t)count | ((uint32_t)b << 8) | ((uint32_t)e << 20);
+}
 
 struct Schedule {
     std::vector<UnitDesc> units_fma, units_mma;
     std::vector<int32_t> tok_row;     // page * P + slot
     std::vector<uint32_t> tok_be;     // b | e << 16
+    std::vector<int32_t> grp_row;     // first pool row of the group (page * P + slot)
+    std::vector<uint32_t> grp_info;   // grp_pack(count, b, e)
     std::vector<int32_t> slot_leaf;   // leaf index
     std::vector<int32_t> slot_part;   // partial id, or -1 - leaf for direct final write
     std::vector<int32_t> merge_leaf;  // leaves merged by the merge kernel

@@ -34,6 +34,14 @@ struct AttnArgs {
     float scale_log2;         // log2(e) / sqrt(D)
     int kv_bf16;
     int out_bf16;
+    // MMA path: TMA tensor maps over the whole K / V pools ([rows][D] bf16,
+    // rows = layer * n_loc * head_rows + head * head_rows + page * P + slot)
+    const void* tmap_k;       // CUtensorMap* (host memory, copied into params)
+    const void* tmap_v;
+    int64_t layer_row0;
+    int64_t head_rows;
+    const int32_t* grp_row;
+    const uint32_t* grp_info;
 };
 
 struct MergeArgs {
@@ -55,6 +63,8 @@ cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, cudaStream_t s);
 // tcgen05/TMEM path (dense bf16 chunks, D in {64,128}).
 cudaError_t launch_attn_mma(const AttnArgs& a, cudaStream_t s);
 bool mma_supported(int D, int kv_bf16);
+// encode the TMA descriptor (128 B, CUtensorMap) of a [rows][D] bf16 pool
+bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D);
 cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s);
 // dst rows[i] <- src row i, for n_loc kv heads: src [n][n_loc][D], dst pool
 cudaError_t launch_kv_scatter(const void* src_k, const void* src_v, void* dst_k, void* dst_v,
