@@ -215,7 +215,7 @@ def main():
     ap.add_argument("--config", default="few_shot", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--graph", type=int, default=1)
+    ap.add_argument("--opt", action="append", default=[], help="ta_set_option key=value (repeatable)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
@@ -261,6 +261,9 @@ def main():
     ctx = TreeAttention(n_layers=L_layers, n_q_heads=h_q, n_kv_heads=h_kv, d_head=d, kv_dtype=cfg["dtype"],
                         out_dtype=cfg["dtype"], max_pages=pages, device=local_rank,
                         kv_head_begin=rank * n_loc, n_local_kv_heads=n_loc)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
     ctx.restore(root, ids, par, cnt)
     dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)

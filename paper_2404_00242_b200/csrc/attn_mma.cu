@@ -261,89 +261,95 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_arrive(BAR(Q_FULL));
 
         float m = -INFINITY, l = 0.f;
+        // warps whose 32 rows are all padding skip the softmax math (they
+        // still take part in every barrier); tcgen05.ld/st are warp-collective
+        const bool warp_live = q4 * 32 < nrows;
         for (int t = 0; t < ntiles; ++t) {
             const int ng = min(8, U.n_grp - 8 * t);
             mbar_wait(BAR(S_FULL), t & 1);
             tc_fence_after();
             float sv[BN];
+            if (warp_live) {
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                if (g < ng) {
-                    uint32_t rr[16];
-                    TMEM_LD16(tmem + lane_addr + TMEM_S + g * 16, rr);
+                for (int g = 0; g < 8; ++g) {
+                    if (g < ng) {
+                        uint32_t rr[16];
+                        TMEM_LD16(tmem + lane_addr + TMEM_S + g * 16, rr);
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) sv[g * 16 + c] = __uint_as_float(rr[c]);
+                        for (int c = 0; c < 16; ++c) sv[g * 16 + c] = __uint_as_float(rr[c]);
+                    }
                 }
+                tmem_wait_ld();
             }
-            tmem_wait_ld();
             tc_fence_before();
             mbar_arrive(BAR(S_FREE));
 
-            // tree mask + scale, row max
             float mx = -INFINITY;
-            const uint32_t* gi = a.grp_info + U.grp_begin + 8 * t;
+            if (warp_live) {
+                // tree mask + scale, row max
+                const uint32_t* gi = a.grp_info + U.grp_begin + 8 * t;
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                if (g < ng) {
-                    const uint32_t info = __ldg(gi + g);
-                    const int cnt = (int)(info & 0xffu), b = (int)((info >> 8) & 0xfffu), e = (int)(info >> 20);
-                    const bool ok = live_row && j >= b && j < e;
+                for (int g = 0; g < 8; ++g) {
+                    if (g < ng) {
+                        const uint32_t info = __ldg(gi + g);
+                        const int cnt = (int)(info & 0xffu), b = (int)((info >> 8) & 0xfffu), e = (int)(info >> 20);
+                        const bool ok = live_row && j >= b && j < e;
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        const float v = (ok && c < cnt) ? sv[g * 16 + c] * a.scale_log2 : -INFINITY;
-                        sv[g * 16 + c] = v;
-                        mx = fmaxf(mx, v);
+                        for (int c = 0; c < 16; ++c) {
+                            const float v = (ok && c < cnt) ? sv[g * 16 + c] * a.scale_log2 : -INFINITY;
+                            sv[g * 16 + c] = v;
+                            mx = fmaxf(mx, v);
+                        }
                     }
                 }
             }
-            // lazy rescale: keep the stale max unless it grew by > kLazy
-            bool waited = false;
-            if (mx > m + kLazy) {
-                if (m != -INFINITY) {
-                    const float f = exp2f(m - mx);
-                    l *= f;
-                    if (t > 0) {
-                        mbar_wait(BAR(O_FULL), (t - 1) & 1);
-                        waited = true;
-                        tc_fence_after();
-#pragma unroll
-                        for (int c = 0; c < DH / 16; ++c) {
-                            uint32_t o[16];
-                            TMEM_LD16(tmem + lane_addr + TMEM_O + c * 16, o);
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
-                            TMEM_ST16(tmem + lane_addr + TMEM_O + c * 16, o);
-                        }
-                        tmem_wait_st();
-                    }
-                }
+            // lazy rescale: keep the stale max unless it grew by > kLazy.  The
+            // O correction is warp-collective (tcgen05.ld/st), so the whole warp
+            // takes the branch when any of its rows needs it (factor 1 otherwise).
+            const bool grow = mx > m + kLazy;
+            float f = 1.f;
+            if (grow) {
+                if (m != -INFINITY) f = exp2f(m - mx);
+                l *= f;
                 m = mx;
             }
-            // the other warps' rows may have rescaled: every thread keeps its
-            // own wait discipline on O_FULL (one wait per tile)
-            if (t > 0 && !waited) mbar_wait(BAR(O_FULL), (t - 1) & 1);
-            // P = exp2(s - m) -> bf16 -> SMEM, l += sum(P)
-            const bool has = m != -INFINITY;
+            if (t > 0) mbar_wait(BAR(O_FULL), (t - 1) & 1);
+            if (t > 0 && __any_sync(0xffffffffu, grow && f != 1.f)) {
+                tc_fence_after();
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                if (g < ng) {
-                    uint32_t pk[8];
+                for (int c = 0; c < DH / 16; ++c) {
+                    uint32_t o[16];
+                    TMEM_LD16(tmem + lane_addr + TMEM_O + c * 16, o);
+                    tmem_wait_ld();
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const float p0 = has ? exp2f(sv[g * 16 + 2 * c] - m) : 0.f;
-                        const float p1 = has ? exp2f(sv[g * 16 + 2 * c + 1] - m) : 0.f;
-                        pk[c] = pack_bf16(p0, p1);
-                        const float2 back = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&pk[c]));
-                        l += back.x + back.y;
-                    }
-                    *reinterpret_cast<uint4*>(smem + SMEM_P + sw128_off(r, 2 * g)) =
-                        make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                    *reinterpret_cast<uint4*>(smem + SMEM_P + sw128_off(r, 2 * g + 1)) =
-                        make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                    for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+                    TMEM_ST16(tmem + lane_addr + TMEM_O + c * 16, o);
                 }
+                tmem_wait_st();
             }
-            fence_proxy_async();
+            if (warp_live) {
+                // P = exp2(s - m) -> bf16 -> SMEM, l += sum(P)
+                const bool has = m != -INFINITY;
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    if (g < ng) {
+                        uint32_t pk[8];
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            const float p0 = has ? exp2f(sv[g * 16 + 2 * c] - m) : 0.f;
+                            const float p1 = has ? exp2f(sv[g * 16 + 2 * c + 1] - m) : 0.f;
+                            pk[c] = pack_bf16(p0, p1);
+                            const float2 back = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&pk[c]));
+                            l += back.x + back.y;
+                        }
+                        *reinterpret_cast<uint4*>(smem + SMEM_P + sw128_off(r, 2 * g)) =
+                            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        *reinterpret_cast<uint4*>(smem + SMEM_P + sw128_off(r, 2 * g + 1)) =
+                            make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                    }
+                }
+                fence_proxy_async();
+            }
             tc_fence_before();
             mbar_arrive(BAR(P_FULL));
         }
@@ -359,6 +365,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (live_row) pid = a.slot_part[U.slot_begin + j];
 #pragma unroll
         for (int c = 0; c < DH / 16; ++c) {
+            if (!warp_live) break;
             uint32_t o[16];
             TMEM_LD16(tmem + lane_addr + TMEM_O + c * 16, o);
             tmem_wait_ld();
