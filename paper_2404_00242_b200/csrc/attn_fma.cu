@@ -375,31 +375,81 @@ cudaError_t launch_fma_d(const AttnArgs& a, cudaStream_t s) {
 // Split-K merge (tree_reduce, attention.hpp:209-233) for leaves covered by
 // more than one unit; partials are consumed in a fixed (unit) order so the
 // result is independent of CTA scheduling.
-__global__ void __launch_bounds__(128) merge_kernel(const MergeArgs a) {
-    const int mi = blockIdx.x;
+__global__ void __launch_bounds__(256) merge_kernel(const MergeArgs a) {
+    // one warp per (merged leaf, q head); lane p fetches partial p's id and
+    // lse (all in flight at once), weights are broadcast by shuffle, and the
+    // O loads of all partials are independent (no dependent-load chain)
+    const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (wid >= a.n_merge * a.hq_loc) return;
+    const int mi = wid / a.hq_loc, hq = wid % a.hq_loc;
     const int leaf = a.merge_leaf[mi];
     const int p0 = a.merge_begin[mi], p1 = a.merge_begin[mi + 1];
-    for (int idx = threadIdx.x; idx < a.hq_loc * a.D; idx += blockDim.x) {
-        const int hq = idx / a.D, d = idx % a.D;
-        float M = -INFINITY;
-        for (int p = p0; p < p1; ++p) M = fmaxf(M, a.part_lse[(size_t)a.merge_parts[p] * a.hq_loc + hq]);
-        float O = 0.f, lse = -INFINITY;
-        if (M != -INFINITY) {
-            float den = 0.f, num = 0.f;
-            for (int p = p0; p < p1; ++p) {
-                const size_t pid = (size_t)a.merge_parts[p];
-                const float lp = a.part_lse[pid * a.hq_loc + hq];
-                if (lp == -INFINITY) continue;
-                const float w = exp2f(lp - M);
-                den += w;
-                num += w * a.part_o[(pid * a.hq_loc + hq) * a.D + d];
-            }
-            O = num / den;
-            lse = (M + log2f(den)) * kLn2;
+    const int D = a.D, dpl = D / 32;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float M = -INFINITY, den = 0.f;
+    for (int base = p0; base < p1; base += 32) {
+        const int np = min(32, p1 - base);
+        int pid = 0;
+        float lp = -INFINITY;
+        if (lane < np) {
+            pid = a.merge_parts[base + lane];
+            lp = a.part_lse[(size_t)pid * a.hq_loc + hq];
         }
-        store_out(a.out, ((size_t)leaf * a.hq_loc + hq) * a.D + d, O, a.out_bf16);
-        if (d == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = lse;
+        float bm = lp;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, off));
+        if (bm == -INFINITY) continue;
+        const float nm = fmaxf(M, bm);
+        const float rescale = M == -INFINITY ? 0.f : exp2f(M - nm);
+        den *= rescale;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] *= rescale;
+        M = nm;
+        const float w = lp == -INFINITY ? 0.f : exp2f(lp - M);
+        float ws = w;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, off);
+        den += ws;
+        if (D >= 32) {
+            int p = 0;
+            for (; p + 4 <= np; p += 4) {
+                float4 v[4];
+                float wv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int id = __shfl_sync(0xffffffffu, pid, p + u);
+                    wv[u] = __shfl_sync(0xffffffffu, w, p + u);
+                    v[u] = *reinterpret_cast<const float4*>(a.part_o + ((size_t)id * a.hq_loc + hq) * D + lane * dpl);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc[0] += wv[u] * v[u].x; acc[1] += wv[u] * v[u].y;
+                    acc[2] += wv[u] * v[u].z; acc[3] += wv[u] * v[u].w;
+                }
+            }
+            for (; p < np; ++p) {
+                const int id = __shfl_sync(0xffffffffu, pid, p);
+                const float wp = __shfl_sync(0xffffffffu, w, p);
+                const float* src = a.part_o + ((size_t)id * a.hq_loc + hq) * D + lane * dpl;
+                for (int i = 0; i < dpl; ++i) acc[i] += wp * src[i];
+            }
+        } else {
+            for (int p = 0; p < np; ++p) {
+                const int id = __shfl_sync(0xffffffffu, pid, p);
+                const float wp = __shfl_sync(0xffffffffu, w, p);
+                if (lane < D) acc[0] += wp * a.part_o[((size_t)id * a.hq_loc + hq) * D + lane];
+            }
+        }
     }
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    const size_t base = ((size_t)leaf * a.hq_loc + hq) * D;
+    if (D >= 32) {
+        for (int i = 0; i < dpl; ++i) store_out(a.out, base + lane * dpl + i, acc[i] * inv, a.out_bf16);
+    } else if (lane < D) {
+        store_out(a.out, base + lane, acc[0] * inv, a.out_bf16);
+    }
+    if (lane == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
 }
 
 // ---------------------------------------------------------------------------
@@ -431,7 +481,8 @@ cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, cudaStream_t s) {
 
 cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s) {
     if (a.n_merge == 0) return cudaSuccess;
-    merge_kernel<<<a.n_merge, 128, 0, s>>>(a);
+    const int warps = a.n_merge * a.hq_loc;
+    merge_kernel<<<(warps + 7) / 8, 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -37,8 +37,12 @@ constexpr int SMEM_Q = 0;
 constexpr int SMEM_P = TILE;
 constexpr int SMEM_KV = 2 * TILE;                        // stage s: K at +s*2*TILE, V at +TILE
 constexpr int SMEM_BAR = SMEM_KV + NSTAGE * 2 * TILE;    // 196608
-constexpr int SMEM_BYTES = SMEM_BAR + 256 + 1024;        // barriers + alignment slack
-constexpr int NTHREADS = 192;
+constexpr int SMEM_RED = SMEM_BAR + 256;                 // [2][128] fp32 row exchange
+constexpr int MAX_GRP = 256;                             // groups per unit held in SMEM (host caps units)
+constexpr int SMEM_GRP = SMEM_RED + 2 * BM * 4;          // [MAX_GRP] row, [MAX_GRP] info
+constexpr int SMEM_TBOX = SMEM_GRP + 2 * MAX_GRP * 4;
+constexpr int SMEM_BYTES = SMEM_TBOX + (MAX_GRP / 8) * 16 + 1024;  // + alignment slack
+constexpr int NTHREADS = 384;
 constexpr int TMEM_COLS = 256;
 constexpr int TMEM_S = 0, TMEM_O = 128;
 constexpr float kLn2 = 0.69314718055994530942f;
@@ -114,6 +118,15 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -126,22 +139,49 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c16) {
     return (uint32_t)(half * HALF + (r >> 3) * 1024 + (r & 7) * 128 + ((ch ^ (r & 7)) << 4));
 }
 
-struct MmaParams {
-    AttnArgs a;
+// Warp roles (384 threads):
+//   warp 0      TMA producer (one lane)
+//   warp 1      QK issuer (one lane); owns the TMEM allocation
+//   warp 2      PV issuer (one lane)
+//   warp 3      idle
+//   warps 4-11  softmax: warp w handles TMEM lane quadrant (w & 3) and the
+//               64-column half h = (w - 4) >> 2 of every S tile, so each row is
+//               shared by two threads (row max exchanged through SMEM).
+// QK and PV are issued by different threads so PV(t) never waits behind the
+// data of tile t+1, and a stage is released as soon as PV(t) has read it.
+constexpr int NSOFT = 256;
+
+// TMA descriptors for boxes of 16, 32, 64, 128 pool rows, K and V.
+struct TmapSet {
+    CUtensorMap k[4];
+    CUtensorMap v[4];
 };
+// trace slots per tile: 0 producer issue, 1 QK: data seen, 2 QK issued, 3 softmax: S seen,
+// 4 softmax: P published, 5 PV issued, 6 producer: stage free seen
+#define TRACE(t, slot)                                                                         \
+    do {                                                                                        \
+        if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && (t) < 64)                          \
+            a.trace[(t) * 8 + (slot)] = clock64();                                              \
+    } while (0)
 
 __global__ void __launch_bounds__(NTHREADS, 1)
-    attn_mma_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-                    const AttnArgs a) {
+    attn_mma_kernel(const __grid_constant__ TmapSet tm, const AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
-    // barriers: full[2], empty[2], s_full, s_free, p_full, o_full, q_full
     const uint32_t bar0 = smem_u32(bars);
     auto BAR = [&](int i) { return bar0 + 8u * (uint32_t)i; };
-    enum { FULL0 = 0, EMPTY0 = 2, S_FULL = 4, S_FREE = 5, P_FULL = 6, O_FULL = 7, Q_FULL = 8 };
+    // K and V have their own full/empty barriers: K(t+2) is loaded as soon as
+    // QK(t) has consumed stage t&1, V(t+2) once PV(t) has.
+    enum { FULLK = 0, FULLV = 2, EMPTYK = 4, EMPTYV = 6, S_FULL = 8, S_FREE = 9, P_FULL = 10, O_FULL = 11,
+           Q_FULL = 12, G_FULL = 13 };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM_BAR + 128);
+    float* red = reinterpret_cast<float*>(smem + SMEM_RED);   // [2][128] row-max halves, then l halves
+    int32_t* g_row = reinterpret_cast<int32_t*>(smem + SMEM_GRP);
+    // per tile: [0] = number of TMA boxes, [1..8] = (first group << 2) | log2(box rows / 16)
+    uint8_t* t_box = smem + SMEM_TBOX;
+    uint32_t* g_info = reinterpret_cast<uint32_t*>(smem + SMEM_GRP + MAX_GRP * 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int kvh = blockIdx.y;
@@ -151,15 +191,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int ntiles = (U.n_grp + 7) >> 3;
 
     if (threadIdx.x == 0) {
-        mbar_init(BAR(FULL0), 1);
-        mbar_init(BAR(FULL0 + 1), 1);
-        mbar_init(BAR(EMPTY0), 1);
-        mbar_init(BAR(EMPTY0 + 1), 1);
+        for (int i = 0; i < 8; ++i) mbar_init(BAR(i), 1);
         mbar_init(BAR(S_FULL), 1);
-        mbar_init(BAR(S_FREE), 128);
-        mbar_init(BAR(P_FULL), 128);
+        mbar_init(BAR(S_FREE), NSOFT);
+        mbar_init(BAR(P_FULL), NSOFT);
         mbar_init(BAR(O_FULL), 1);
-        mbar_init(BAR(Q_FULL), 128);
+        mbar_init(BAR(Q_FULL), NSOFT);
+        mbar_init(BAR(G_FULL), 32);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
@@ -172,37 +210,56 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    long long t_begin = 0;
+    if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
 
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                asm volatile("prefetch.tensormap [%0];" ::"l"(&tm.k[i]) : "memory");
+                asm volatile("prefetch.tensormap [%0];" ::"l"(&tm.v[i]) : "memory");
+            }
             const int64_t row0 = a.layer_row0 + (int64_t)kvh * a.head_rows;
+            mbar_wait(BAR(G_FULL), 0);
             for (int t = 0; t < ntiles; ++t) {
                 const int s = t & 1;
-                mbar_wait(BAR(EMPTY0 + s), ((t >> 1) & 1) ^ 1);
                 const int ng = min(8, U.n_grp - 8 * t);
-                mbar_expect_tx(BAR(FULL0 + s), (uint32_t)ng * 4u * 2048u);
                 const uint32_t kdst = sbase + SMEM_KV + (uint32_t)s * 2 * TILE;
                 const uint32_t vdst = kdst + TILE;
-                for (int g = 0; g < ng; ++g) {
-                    const int row = (int)(row0 + a.grp_row[U.grp_begin + 8 * t + g]);
-                    tma_load_2d(kdst + g * 2048, &tmk, 0, row, BAR(FULL0 + s));
-                    tma_load_2d(kdst + HALF + g * 2048, &tmk, 64, row, BAR(FULL0 + s));
-                    tma_load_2d(vdst + g * 2048, &tmv, 0, row, BAR(FULL0 + s));
-                    tma_load_2d(vdst + HALF + g * 2048, &tmv, 64, row, BAR(FULL0 + s));
+                const uint8_t* bx = t_box + 16 * t;
+                const int nb = bx[0];
+                const uint32_t bytes = (uint32_t)ng * 2u * 2048u;
+                mbar_wait(BAR(EMPTYK + s), ((t >> 1) & 1) ^ 1);
+                TRACE(t, 6);
+                mbar_expect_tx(BAR(FULLK + s), bytes);
+                for (int b = 0; b < nb; ++b) {
+                    const int g = bx[1 + b] >> 2, sz = bx[1 + b] & 3;
+                    const int row = (int)(row0 + g_row[8 * t + g]);
+                    tma_load_2d(kdst + g * 2048, &tm.k[sz], 0, row, BAR(FULLK + s));
+                    tma_load_2d(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s));
                 }
+                mbar_wait(BAR(EMPTYV + s), ((t >> 1) & 1) ^ 1);
+                mbar_expect_tx(BAR(FULLV + s), bytes);
+                for (int b = 0; b < nb; ++b) {
+                    const int g = bx[1 + b] >> 2, sz = bx[1 + b] & 3;
+                    const int row = (int)(row0 + g_row[8 * t + g]);
+                    tma_load_2d(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + s));
+                    tma_load_2d(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + s));
+                }
+                TRACE(t, 0);
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer =====================
+        // ===================== QK issuer: S = Q K^T =====================
         if (lane == 0) {
-            const uint32_t sQ = sbase + SMEM_Q, sP = sbase + SMEM_P;
-            const uint32_t tS = tmem + TMEM_S, tO = tmem + TMEM_O;
+            const uint32_t sQ = sbase + SMEM_Q;
             mbar_wait(BAR(Q_FULL), 0);
-            tc_fence_after();
-            auto issue_qk = [&](int t) {
+            for (int t = 0; t < ntiles; ++t) {
                 const int s = t & 1;
-                mbar_wait(BAR(FULL0 + s), (t >> 1) & 1);
+                mbar_wait(BAR(FULLK + s), (t >> 1) & 1);
+                TRACE(t, 1);
                 if (t > 0) mbar_wait(BAR(S_FREE), (t - 1) & 1);
                 tc_fence_after();
                 const int ng = min(8, U.n_grp - 8 * t);
@@ -211,14 +268,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                 for (int k = 0; k < DH / 16; ++k) {
                     const uint32_t off = (uint32_t)((k >> 2) * HALF + (k & 3) * 32);
-                    mma_bf16(tS, sdesc(sQ + off, 16, 1024), sdesc(sK + off, 16, 1024), id, k > 0);
+                    mma_bf16(tmem + TMEM_S, sdesc(sQ + off, 16, 1024), sdesc(sK + off, 16, 1024), id, k > 0);
                 }
                 mma_commit(BAR(S_FULL));
-            };
-            if (ntiles > 0) issue_qk(0);
+                mma_commit(BAR(EMPTYK + s));
+                TRACE(t, 2);
+            }
+        }
+    } else if (warp == 2) {
+        // ===================== PV issuer: O += P V =====================
+        if (lane == 0) {
+            const uint32_t sP = sbase + SMEM_P;
             for (int t = 0; t < ntiles; ++t) {
                 const int s = t & 1;
-                if (t + 1 < ntiles) issue_qk(t + 1);
+                mbar_wait(BAR(FULLV + s), (t >> 1) & 1);
                 mbar_wait(BAR(P_FULL), t & 1);
                 tc_fence_after();
                 const int ng = min(8, U.n_grp - 8 * t);
@@ -226,25 +289,58 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const uint32_t id = idesc_bf16(BM, DH, 0, 1);
                 for (int kk = 0; kk < ng; ++kk) {
                     const uint32_t poff = (uint32_t)((kk >> 2) * HALF + (kk & 3) * 32);
-                    mma_bf16(tO, sdesc(sP + poff, 16, 1024), sdesc(sV + kk * 2048, HALF, 1024), id,
+                    mma_bf16(tmem + TMEM_O, sdesc(sP + poff, 16, 1024), sdesc(sV + kk * 2048, HALF, 1024), id,
                              (t > 0 || kk > 0) ? 1u : 0u);
                 }
-                mma_commit(BAR(EMPTY0 + s));
+                mma_commit(BAR(EMPTYV + s));
                 mma_commit(BAR(O_FULL));
+                TRACE(t, 5);
             }
         }
-    } else {
-        // ===================== softmax / epilogue (128 threads) =====================
+    } else if (warp == 3) {
+        // ===================== group metadata -> SMEM (once per unit) =====================
+        for (int g = lane; g < U.n_grp; g += 32) {
+            g_row[g] = a.grp_row[U.grp_begin + g];
+            g_info[g] = a.grp_info[U.grp_begin + g];
+        }
+        __syncwarp();
+        // box plan per tile: runs of full, row-contiguous groups are loaded as
+        // power-of-two boxes (8/4/2/1 groups); the box bytes always
+        // equal 16 rows per group (masked rows are never read)
+        for (int t = lane; t < ntiles; t += 32) {
+            const int ng = min(8, U.n_grp - 8 * t);
+            uint8_t* bx = t_box + 16 * t;
+            int nb = 0, g = 0;
+            while (g < ng) {
+                int run = 1;  // full contiguous groups starting at g (the last may be partial)
+                while (g + run < ng && (g_info[8 * t + g + run - 1] & 0xffu) == 16u &&
+                       g_row[8 * t + g + run] == g_row[8 * t + g] + 16 * run)
+                    ++run;
+                while (run > 0) {
+                    int sz = 3;
+                    while ((1 << sz) > run) --sz;
+                    bx[1 + nb++] = (uint8_t)((g << 2) | sz);
+                    g += 1 << sz;
+                    run -= 1 << sz;
+                }
+            }
+            bx[0] = (uint8_t)nb;
+        }
+        __syncwarp();
+        mbar_arrive(BAR(G_FULL));
+    } else if (warp >= 4) {
+        // ===================== softmax / epilogue (256 threads) =====================
         const int q4 = warp & 3;                 // TMEM lane quadrant of this warp
+        const int h = (warp - 4) >> 2;           // column half (S groups 4h..4h+3, O cols 64h..)
         const int r = q4 * 32 + lane;            // row == TMEM lane
         const bool live_row = r < nrows;
         const int j = live_row ? r / G : -1;     // local query slot
         const int hq = kvh * G + (live_row ? r % G : 0);
         const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
+        const bool warp_live = q4 * 32 < nrows;
 
-        // Q row -> SMEM (K-major SW128); zeros for padding rows
+        // Q row -> SMEM (K-major SW128); this thread writes 8 of the 16 chunks
         {
-            uint4 z = make_uint4(0, 0, 0, 0);
             const uint4* src = nullptr;
             if (live_row) {
                 const int leaf = a.slot_leaf[U.slot_begin + j];
@@ -252,29 +348,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                                      ((size_t)leaf * a.hq_loc + hq) * DH);
             }
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                const uint4 v = live_row ? src[c] : z;
-                *reinterpret_cast<uint4*>(smem + SMEM_Q + sw128_off(r, c)) = v;
+            for (int c = 8 * h; c < 8 * h + 8; ++c) {
+                const uint4 v = live_row ? src[c] : make_uint4(0, 0, 0, 0);
+                sts128(sbase + SMEM_Q + sw128_off(r, c), v.x, v.y, v.z, v.w);
             }
         }
         fence_proxy_async();
         mbar_arrive(BAR(Q_FULL));
 
         float m = -INFINITY, l = 0.f;
-        // warps whose 32 rows are all padding skip the softmax math (they
-        // still take part in every barrier); tcgen05.ld/st are warp-collective
-        const bool warp_live = q4 * 32 < nrows;
+        const float sc = a.scale_log2;
+        mbar_wait(BAR(G_FULL), 0);
         for (int t = 0; t < ntiles; ++t) {
             const int ng = min(8, U.n_grp - 8 * t);
+            const int g0 = 4 * h;
             mbar_wait(BAR(S_FULL), t & 1);
+            if (threadIdx.x == 128) TRACE(t, 3);
             tc_fence_after();
-            float sv[BN];
+            float sv[64];
             if (warp_live) {
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    if (g < ng) {
+                for (int g = 0; g < 4; ++g) {
+                    if (g0 + g < ng) {
                         uint32_t rr[16];
-                        TMEM_LD16(tmem + lane_addr + TMEM_S + g * 16, rr);
+                        TMEM_LD16(tmem + lane_addr + TMEM_S + (g0 + g) * 16, rr);
 #pragma unroll
                         for (int c = 0; c < 16; ++c) sv[g * 16 + c] = __uint_as_float(rr[c]);
                     }
@@ -284,32 +381,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc_fence_before();
             mbar_arrive(BAR(S_FREE));
 
+            // tree mask on the raw scores (scale > 0 commutes with max)
             float mx = -INFINITY;
             if (warp_live) {
-                // tree mask + scale, row max
-                const uint32_t* gi = a.grp_info + U.grp_begin + 8 * t;
+                const uint32_t* gi = g_info + 8 * t + g0;
+                float mxa[4];
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    if (g < ng) {
-                        const uint32_t info = __ldg(gi + g);
+                for (int g = 0; g < 4; ++g) {
+                    mxa[g] = -INFINITY;
+                    if (g0 + g < ng) {
+                        const uint32_t info = gi[g];
                         const int cnt = (int)(info & 0xffu), b = (int)((info >> 8) & 0xfffu), e = (int)(info >> 20);
-                        const bool ok = live_row && j >= b && j < e;
+                        const int lim = (live_row && j >= b && j < e) ? cnt : 0;
 #pragma unroll
                         for (int c = 0; c < 16; ++c) {
-                            const float v = (ok && c < cnt) ? sv[g * 16 + c] * a.scale_log2 : -INFINITY;
+                            const float v = c < lim ? sv[g * 16 + c] : -INFINITY;
                             sv[g * 16 + c] = v;
-                            mx = fmaxf(mx, v);
+                            mxa[g] = fmaxf(mxa[g], v);
                         }
                     }
                 }
+                mx = fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3]));
             }
-            // lazy rescale: keep the stale max unless it grew by > kLazy.  The
-            // O correction is warp-collective (tcgen05.ld/st), so the whole warp
-            // takes the branch when any of its rows needs it (factor 1 otherwise).
+            // combine the two halves of the row
+            red[h * BM + r] = mx;
+            asm volatile("bar.sync 1, %0;" ::"n"(NSOFT) : "memory");
+            mx = fmaxf(mx, red[(h ^ 1) * BM + r]) * sc;
+            // lazy rescale: keep the stale max unless it grew by > kLazy (both
+            // threads of a row take the same decision).  The O correction is
+            // warp-collective, so a warp takes it when any of its rows needs it.
             const bool grow = mx > m + kLazy;
             float f = 1.f;
             if (grow) {
-                if (m != -INFINITY) f = exp2f(m - mx);
+                if (m != -INFINITY) f = ex2(m - mx);
                 l *= f;
                 m = mx;
             }
@@ -317,89 +421,99 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (t > 0 && __any_sync(0xffffffffu, grow && f != 1.f)) {
                 tc_fence_after();
 #pragma unroll
-                for (int c = 0; c < DH / 16; ++c) {
+                for (int c = 0; c < 4; ++c) {
                     uint32_t o[16];
-                    TMEM_LD16(tmem + lane_addr + TMEM_O + c * 16, o);
+                    TMEM_LD16(tmem + lane_addr + TMEM_O + h * 64 + c * 16, o);
                     tmem_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
-                    TMEM_ST16(tmem + lane_addr + TMEM_O + c * 16, o);
+                    TMEM_ST16(tmem + lane_addr + TMEM_O + h * 64 + c * 16, o);
                 }
                 tmem_wait_st();
             }
             if (warp_live) {
-                // P = exp2(s - m) -> bf16 -> SMEM, l += sum(P)
-                const bool has = m != -INFINITY;
+                // P = exp2(s * scale - m) -> bf16 -> SMEM; l += sum(P)
+                const float negm = m == -INFINITY ? 0.f : -m;
+                float la[4];
+                const uint32_t prow = sbase + SMEM_P;
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    if (g < ng) {
+                for (int g = 0; g < 4; ++g) {
+                    la[g] = 0.f;
+                    if (g0 + g < ng) {
                         uint32_t pk[8];
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
-                            const float p0 = has ? exp2f(sv[g * 16 + 2 * c] - m) : 0.f;
-                            const float p1 = has ? exp2f(sv[g * 16 + 2 * c + 1] - m) : 0.f;
+                            const float p0 = ex2(fmaf(sv[g * 16 + 2 * c], sc, negm));
+                            const float p1 = ex2(fmaf(sv[g * 16 + 2 * c + 1], sc, negm));
+                            la[g] += p0 + p1;
                             pk[c] = pack_bf16(p0, p1);
-                            const float2 back = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&pk[c]));
-                            l += back.x + back.y;
                         }
-                        *reinterpret_cast<uint4*>(smem + SMEM_P + sw128_off(r, 2 * g)) =
-                            make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                        *reinterpret_cast<uint4*>(smem + SMEM_P + sw128_off(r, 2 * g + 1)) =
-                            make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                        sts128(prow + sw128_off(r, 2 * (g0 + g)), pk[0], pk[1], pk[2], pk[3]);
+                        sts128(prow + sw128_off(r, 2 * (g0 + g) + 1), pk[4], pk[5], pk[6], pk[7]);
                     }
                 }
+                l += (la[0] + la[1]) + (la[2] + la[3]);
                 fence_proxy_async();
             }
             tc_fence_before();
             mbar_arrive(BAR(P_FULL));
+            if (threadIdx.x == 128) TRACE(t, 4);
         }
 
-        // epilogue: O / l -> partial or final output
+        // epilogue: O / l -> partial or final output (this thread: 64 columns)
         if (ntiles > 0) {
             mbar_wait(BAR(O_FULL), (ntiles - 1) & 1);
             tc_fence_after();
         }
+        asm volatile("bar.sync 1, %0;" ::"n"(NSOFT) : "memory");  // red[] reuse
+        red[h * BM + r] = l;
+        asm volatile("bar.sync 1, %0;" ::"n"(NSOFT) : "memory");
+        l += red[(h ^ 1) * BM + r];
         const float inv = (live_row && l > 0.f) ? 1.f / l : 0.f;
         const float lse2 = m + log2f(l);
         int pid = 0;
         if (live_row) pid = a.slot_part[U.slot_begin + j];
+        if (warp_live) {
 #pragma unroll
-        for (int c = 0; c < DH / 16; ++c) {
-            if (!warp_live) break;
-            uint32_t o[16];
-            TMEM_LD16(tmem + lane_addr + TMEM_O + c * 16, o);
-            tmem_wait_ld();
-            if (live_row) {
-                if (pid < 0) {
-                    const int leaf = -1 - pid;
-                    const size_t base = ((size_t)leaf * a.hq_loc + hq) * DH + c * 16;
-                    if (a.out_bf16) {
-                        uint4 w0, w1;
-                        uint32_t* p0 = &w0.x;
-                        uint32_t* p1 = &w1.x;
+            for (int c = 0; c < 4; ++c) {
+                uint32_t o[16];
+                const int col = h * 64 + c * 16;
+                TMEM_LD16(tmem + lane_addr + TMEM_O + col, o);
+                tmem_wait_ld();
+                if (live_row) {
+                    if (pid < 0) {
+                        const int leaf = -1 - pid;
+                        const size_t base = ((size_t)leaf * a.hq_loc + hq) * DH + col;
+                        if (a.out_bf16) {
+                            uint4 w0, w1;
+                            uint32_t* p0 = &w0.x;
+                            uint32_t* p1 = &w1.x;
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            p0[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-                            p1[i] = pack_bf16(__uint_as_float(o[8 + 2 * i]) * inv, __uint_as_float(o[9 + 2 * i]) * inv);
+                            for (int i = 0; i < 4; ++i) {
+                                p0[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
+                                p1[i] = pack_bf16(__uint_as_float(o[8 + 2 * i]) * inv,
+                                                  __uint_as_float(o[9 + 2 * i]) * inv);
+                            }
+                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + base);
+                            dst[0] = w0;
+                            dst[1] = w1;
+                        } else {
+                            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + base);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
+                                                     __uint_as_float(o[4 * i + 2]) * inv,
+                                                     __uint_as_float(o[4 * i + 3]) * inv);
                         }
-                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + base);
-                        dst[0] = w0;
-                        dst[1] = w1;
+                        if (c == 0 && h == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = lse2 * kLn2;
                     } else {
-                        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + base);
+                        float4* dst = reinterpret_cast<float4*>(a.part_o + ((size_t)pid * a.hq_loc + hq) * DH + col);
 #pragma unroll
                         for (int i = 0; i < 4; ++i)
                             dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
                                                  __uint_as_float(o[4 * i + 2]) * inv, __uint_as_float(o[4 * i + 3]) * inv);
+                        if (c == 0 && h == 0) a.part_lse[(size_t)pid * a.hq_loc + hq] = lse2;
                     }
-                    if (c == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = lse2 * kLn2;
-                } else {
-                    float4* dst = reinterpret_cast<float4*>(a.part_o + ((size_t)pid * a.hq_loc + hq) * DH + c * 16);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
-                                             __uint_as_float(o[4 * i + 2]) * inv, __uint_as_float(o[4 * i + 3]) * inv);
-                    if (c == 0) a.part_lse[(size_t)pid * a.hq_loc + hq] = lse2;
                 }
             }
         }
@@ -407,6 +521,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (a.trace && threadIdx.x == 0) {
+        long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+        if (cta < 4096) {
+            unsigned smid;
+            asm("mov.u32 %0, %%smid;" : "=r"(smid));
+            a.trace[512 + 4 * cta] = t_begin;
+            a.trace[512 + 4 * cta + 1] = t_end;
+            a.trace[512 + 4 * cta + 2] = smid;
+            a.trace[512 + 4 * cta + 3] = ((long long)U.n_grp << 32) | (unsigned)nrows;
+        }
+    }
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
@@ -417,7 +544,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 bool mma_supported(int D, int kv_bf16) { return kv_bf16 && D == DH; }
 
-bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D) {
+bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D, int box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -430,7 +557,7 @@ bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D) {
     CUtensorMap* m = reinterpret_cast<CUtensorMap*>(tmap_out);
     const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-    const cuuint32_t box[2] = {64, 16};
+    const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -447,11 +574,11 @@ cudaError_t launch_attn_mma(const AttnArgs& a, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    CUtensorMap tk, tv;
-    std::memcpy(&tk, a.tmap_k, sizeof(CUtensorMap));
-    std::memcpy(&tv, a.tmap_v, sizeof(CUtensorMap));
+    TmapSet tm;
+    std::memcpy(tm.k, a.tmap_k, sizeof(tm.k));
+    std::memcpy(tm.v, a.tmap_v, sizeof(tm.v));
     dim3 grid(a.n_units, a.n_kv_loc);
-    attn_mma_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(tk, tv, a);
+    attn_mma_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(tm, a);
     return cudaGetLastError();
 }
 

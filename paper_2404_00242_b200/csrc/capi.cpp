@@ -35,8 +35,8 @@ struct ta_ctx {
     int prepared_bs = -1;
 
     // TMA descriptors (CUtensorMap, 128 B) over the whole K / V pools
-    alignas(64) unsigned char tmap_k[128];
-    alignas(64) unsigned char tmap_v[128];
+    alignas(64) unsigned char tmap_k[512];   // CUtensorMap for 16/32/64/128-row boxes
+    alignas(64) unsigned char tmap_v[512];
     bool tmaps_ok = false;
 
     // device pools: one K and one V slab per layer, [n_loc][max_pages][P][D]
@@ -206,8 +206,10 @@ ta_status ta_ctx_create(int device, const ta_shape* s, ta_ctx** out) {
             c->opt.num_sms = prop.multiProcessorCount;
             if (mma_supported(sh.d_head, sh.kv_dtype == TA_BF16)) {
                 const int64_t rows = (int64_t)sh.n_layers * sh.n_local_kv_heads * sh.max_pages * sh.page_tokens;
-                c->tmaps_ok = make_pool_tmap(c->tmap_k, c->kv_k, rows, sh.d_head) &&
-                              make_pool_tmap(c->tmap_v, c->kv_v, rows, sh.d_head);
+                c->tmaps_ok = true;
+                for (int i = 0; i < 4; ++i)
+                    c->tmaps_ok = c->tmaps_ok && make_pool_tmap(c->tmap_k + 128 * i, c->kv_k, rows, sh.d_head, 16 << i) &&
+                                  make_pool_tmap(c->tmap_v + 128 * i, c->kv_v, rows, sh.d_head, 16 << i);
                 if (!c->tmaps_ok) fail(TA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the KV pools");
             }
         }
@@ -236,6 +238,8 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->opt.span_tokens = (int)v;
         } else if (k == "final_direct") {
             c->opt.final_direct = v != 0;
+        } else if (k == "trace_ptr") {
+            c->opt.trace_ptr = v;
         } else if (k == "num_sms") {
             c->opt.num_sms = (int)v;
         } else {
@@ -521,6 +525,7 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.layer_row0 = (int64_t)layer * c->shape.n_local_kv_heads * a.head_rows;
     a.grp_row = c->d_grp_row;
     a.grp_info = c->d_grp_info;
+    a.trace = reinterpret_cast<long long*>(c->opt.trace_ptr);
     if (!S.units_fma.empty()) {
         a.units = c->d_units_fma;
         a.n_units = (int)S.units_fma.size();

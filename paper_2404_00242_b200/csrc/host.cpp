@@ -430,10 +430,13 @@ struct Piece {
     int32_t lo, hi;
 };
 
+constexpr int kMaxUnitGroups = 256;  // = MAX_GRP of attn_mma.cu
+
 struct OpenUnit {
     std::vector<int32_t> slots;  // sorted leaf indices
     std::vector<Piece> pieces;
     int64_t tokens = 0;
+    int64_t grp_est = 0;         // upper bound on 16-row TMA groups
     int last_chunk = -1;
     bool mma = false;
 };
@@ -458,6 +461,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
         int q0, q1;  // into plan.chunk_q
         bool mma;
         int64_t tokens;
+        int64_t grp_est;
     };
     std::vector<Block> blocks;
     int64_t work_tokens = 0;
@@ -473,11 +477,13 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
         for (int k = 0; k < nb; ++k) {
             const int a = qb + (int)((int64_t)nq * k / nb);
             const int b = qb + (int)((int64_t)nq * (k + 1) / nb);
-            int64_t toks = 0;
+            int64_t toks = 0, grp = 0;
             for (int s = plan.chunk_seg_begin[c]; s < plan.chunk_seg_begin[c + 1]; ++s)
-                if (plan.cseg_hi[s] > plan.chunk_q[a] && plan.cseg_lo[s] <= plan.chunk_q[b - 1])
+                if (plan.cseg_hi[s] > plan.chunk_q[a] && plan.cseg_lo[s] <= plan.chunk_q[b - 1]) {
                     toks += plan.cseg_len[s];
-            blocks.push_back({c, a, b, mma, toks});
+                    grp += (plan.cseg_len[s] + 15) / 16 + 1;
+                }
+            blocks.push_back({c, a, b, mma, toks, grp});
             work_tokens += toks;
         }
         for (int s = plan.chunk_seg_begin[c]; s < plan.chunk_seg_begin[c + 1]; ++s)
@@ -515,6 +521,8 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
             OpenUnit& u = open[i];
             if (u.mma != bl.mma || u.last_chunk != bl.chunk - 1) continue;
             if (u.tokens + bl.tokens > span) continue;
+            // MMA units keep their group metadata in SMEM: <= kMaxUnitGroups boxes
+            if (u.mma && u.grp_est + bl.grp_est > kMaxUnitGroups) continue;
             sorted_union(u.slots, bq, nb, tmp);
             if ((int)tmp.size() > S_slots) continue;
             // prefer exact continuation of the same query block
@@ -539,6 +547,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                                     std::max(plan.cseg_lo[s], bq[0]), std::min(plan.cseg_hi[s], bq[nb - 1] + 1)});
                 u.tokens += plan.cseg_len[s];
             }
+        u.grp_est += bl.grp_est;
         u.last_chunk = bl.chunk;
     }
     for (auto& u : open) done.push_back(std::move(u));
@@ -591,6 +600,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                 k += cnt;
             }
             d.n_grp = (int32_t)S.grp_row.size() - d.grp_begin;
+            if (d.n_grp > kMaxUnitGroups) fail(TA_ERR_LOGIC, "schedule: MMA unit exceeds its group capacity");
             S.kv_tokens_loaded += 16LL * d.n_grp - d.n_tokens;  // box over-read
         }
         dst.push_back(d);

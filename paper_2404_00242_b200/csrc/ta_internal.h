@@ -170,6 +170,7 @@ struct SchedOptions {
     int span_tokens = 0;       // 0 = auto
     bool final_direct = true;  // single-partial leaves written directly
     int num_sms = 148;
+    int64_t trace_ptr = 0;     // debug: device buffer for the MMA kernel's clock64 trace
 };
 
 void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int group_size,

@@ -36,12 +36,13 @@ struct AttnArgs {
     int out_bf16;
     // MMA path: TMA tensor maps over the whole K / V pools ([rows][D] bf16,
     // rows = layer * n_loc * head_rows + head * head_rows + page * P + slot)
-    const void* tmap_k;       // CUtensorMap* (host memory, copied into params)
+    const void* tmap_k;       // CUtensorMap[4] (16/32/64/128-row boxes; host memory, copied into params)
     const void* tmap_v;
     int64_t layer_row0;
     int64_t head_rows;
     const int32_t* grp_row;
     const uint32_t* grp_info;
+    long long* trace;         // optional per-tile clock64 trace of CTA (0,0)
 };
 
 struct MergeArgs {
@@ -64,7 +65,7 @@ cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, cudaStream_t s);
 cudaError_t launch_attn_mma(const AttnArgs& a, cudaStream_t s);
 bool mma_supported(int D, int kv_bf16);
 // encode the TMA descriptor (128 B, CUtensorMap) of a [rows][D] bf16 pool
-bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D);
+bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D, int box_rows);
 cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s);
 // dst rows[i] <- src row i, for n_loc kv heads: src [n][n_loc][D], dst pool
 cudaError_t launch_kv_scatter(const void* src_k, const void* src_v, void* dst_k, void* dst_v,
