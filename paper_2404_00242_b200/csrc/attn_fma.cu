@@ -375,18 +375,36 @@ cudaError_t launch_fma_d(const AttnArgs& a, cudaStream_t s) {
 // Split-K merge (tree_reduce, attention.hpp:209-233) for leaves covered by
 // more than one unit; partials are consumed in a fixed (unit) order so the
 // result is independent of CTA scheduling.
+template <int DPL>
+__device__ __forceinline__ void load_dpl(const float* p, float (&f)[DPL]) {
+    if constexpr (DPL == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(p);
+        f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+    } else if constexpr (DPL == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(p);
+        f[0] = v.x; f[1] = v.y;
+    } else {
+        f[0] = p[0];
+    }
+}
+
+// one warp per (merged leaf, q head); lane p fetches partial p's id and lse
+// (all in flight at once), weights are broadcast by shuffle, and the O loads
+// of all partials are independent (no dependent-load chain).  Lane i owns
+// output dims [i*DPL, (i+1)*DPL) (D < 32: lanes >= D idle).
+template <int DPL>
 __global__ void __launch_bounds__(256) merge_kernel(const MergeArgs a) {
-    // one warp per (merged leaf, q head); lane p fetches partial p's id and
-    // lse (all in flight at once), weights are broadcast by shuffle, and the
-    // O loads of all partials are independent (no dependent-load chain)
     const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (wid >= a.n_merge * a.hq_loc) return;
     const int mi = wid / a.hq_loc, hq = wid % a.hq_loc;
     const int leaf = a.merge_leaf[mi];
     const int p0 = a.merge_begin[mi], p1 = a.merge_begin[mi + 1];
-    const int D = a.D, dpl = D / 32;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int D = a.D;
+    const bool active = lane * DPL < D;
+    float acc[DPL];
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
     float M = -INFINITY, den = 0.f;
     for (int base = p0; base < p1; base += 32) {
         const int np = min(32, p1 - base);
@@ -404,51 +422,45 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeArgs a) {
         const float rescale = M == -INFINITY ? 0.f : exp2f(M - nm);
         den *= rescale;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i] *= rescale;
+        for (int i = 0; i < DPL; ++i) acc[i] *= rescale;
         M = nm;
         const float w = lp == -INFINITY ? 0.f : exp2f(lp - M);
         float ws = w;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, off);
         den += ws;
-        if (D >= 32) {
-            int p = 0;
-            for (; p + 4 <= np; p += 4) {
-                float4 v[4];
-                float wv[4];
+        int p = 0;
+        for (; p + 4 <= np; p += 4) {
+            float v[4][DPL];
+            float wv[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int id = __shfl_sync(0xffffffffu, pid, p + u);
-                    wv[u] = __shfl_sync(0xffffffffu, w, p + u);
-                    v[u] = *reinterpret_cast<const float4*>(a.part_o + ((size_t)id * a.hq_loc + hq) * D + lane * dpl);
-                }
+            for (int u = 0; u < 4; ++u) {
+                const int id = __shfl_sync(0xffffffffu, pid, p + u);
+                wv[u] = __shfl_sync(0xffffffffu, w, p + u);
+                if (active) load_dpl<DPL>(a.part_o + ((size_t)id * a.hq_loc + hq) * D + lane * DPL, v[u]);
+            }
+            if (active)
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    acc[0] += wv[u] * v[u].x; acc[1] += wv[u] * v[u].y;
-                    acc[2] += wv[u] * v[u].z; acc[3] += wv[u] * v[u].w;
-                }
-            }
-            for (; p < np; ++p) {
-                const int id = __shfl_sync(0xffffffffu, pid, p);
-                const float wp = __shfl_sync(0xffffffffu, w, p);
-                const float* src = a.part_o + ((size_t)id * a.hq_loc + hq) * D + lane * dpl;
-                for (int i = 0; i < dpl; ++i) acc[i] += wp * src[i];
-            }
-        } else {
-            for (int p = 0; p < np; ++p) {
-                const int id = __shfl_sync(0xffffffffu, pid, p);
-                const float wp = __shfl_sync(0xffffffffu, w, p);
-                if (lane < D) acc[0] += wp * a.part_o[((size_t)id * a.hq_loc + hq) * D + lane];
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int i = 0; i < DPL; ++i) acc[i] += wv[u] * v[u][i];
+        }
+        for (; p < np; ++p) {
+            const int id = __shfl_sync(0xffffffffu, pid, p);
+            const float wp = __shfl_sync(0xffffffffu, w, p);
+            if (active) {
+                float v[DPL];
+                load_dpl<DPL>(a.part_o + ((size_t)id * a.hq_loc + hq) * D + lane * DPL, v);
+#pragma unroll
+                for (int i = 0; i < DPL; ++i) acc[i] += wp * v[i];
             }
         }
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;
     const size_t base = ((size_t)leaf * a.hq_loc + hq) * D;
-    if (D >= 32) {
-        for (int i = 0; i < dpl; ++i) store_out(a.out, base + lane * dpl + i, acc[i] * inv, a.out_bf16);
-    } else if (lane < D) {
-        store_out(a.out, base + lane, acc[0] * inv, a.out_bf16);
-    }
+    if (active)
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) store_out(a.out, base + lane * DPL + i, acc[i] * inv, a.out_bf16);
     if (lane == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
 }
 
@@ -482,7 +494,10 @@ cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, cudaStream_t s) {
 cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s) {
     if (a.n_merge == 0) return cudaSuccess;
     const int warps = a.n_merge * a.hq_loc;
-    merge_kernel<<<(warps + 7) / 8, 256, 0, s>>>(a);
+    const int blocks = (warps + 7) / 8;
+    if (a.D >= 128) merge_kernel<4><<<blocks, 256, 0, s>>>(a);
+    else if (a.D >= 64) merge_kernel<2><<<blocks, 256, 0, s>>>(a);
+    else merge_kernel<1><<<blocks, 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 
