@@ -76,7 +76,8 @@ int ta_abi_version(void);
 /* device < 0 creates a host-only context (tree, page accounting, planner). */
 ta_status ta_ctx_create(int device, const ta_shape* shape, ta_ctx** out);
 ta_status ta_ctx_destroy(ta_ctx* ctx);
-/* tuning knobs: "fma_max_rows", "use_mma", "span_tokens", "final_direct" */
+/* tuning knobs: "use_mma", "fma_max_rows", "mma_max_rows", "tile_groups",
+ * "tile_cost", "num_ctas", "final_direct", "pdl" */
 ta_status ta_set_option(ta_ctx* ctx, const char* key, int64_t value);
 
 /* ---- DecodingTree (tree mutations drive the page pool like KvLifecycle) -- */
@@ -151,8 +152,8 @@ ta_status ta_attend_host(ta_ctx* ctx, int layer, const void* q_host, void* out_h
 typedef struct ta_io_stats {
     int64_t n_chunks;          /* flatten chunks (sibling groups fused) */
     int64_t n_groups;          /* reference QkvGroups */
-    int64_t n_units;           /* CTA work units per kv head */
-    int64_t n_units_mma;
+    int64_t n_units;           /* items (CTA work runs, all local kv heads) */
+    int64_t n_units_mma;       /* items run by the tcgen05 kernel */
     int64_t n_partials;        /* (unit, query) partial records per kv head */
     int64_t kv_bytes;          /* unique KV bytes read per layer (this shard) */
     int64_t kv_bytes_loaded;   /* KV bytes the schedule loads (incl. row-block re-reads) */
@@ -165,25 +166,41 @@ typedef struct ta_io_stats {
 ta_status ta_io_stats_get(ta_ctx* ctx, ta_io_stats* out);
 
 /* Device schedule of the current tree (built on the host; works on host-only
- * contexts).  Unit u of kind k (0 = FMA, 1 = MMA) covers tokens
- * [tok_begin, tok_begin+n_tokens) of tok_row/tok_be and slots
- * [slot_begin, slot_begin+n_slots) of slot_leaf/slot_part.  tok_row =
- * page * page_tokens + slot; tok_be = b | e << 16: local slots [b, e) attend.
- * slot_part >= 0: partial id merged in merge order; < 0: -1-leaf, written
- * directly.  Arrays stay valid until the next schedule/prepare call. */
+ * contexts; layout described in DESIGN.md section 3).  CTA c runs items
+ * [cta_begin[c], cta_begin[c+1]).  items: [n_items][8] int32 = {head,
+ * tile_begin, tile_end, slot_begin, n_slots, out_begin, lane, flags}.
+ * tiles: [n_tiles][4] int32 = raw 16-byte tile records {grp_begin,
+ * ng | nbox << 8 | ntok << 16, boxes 0-3, boxes 4-7}.  Group g covers
+ * (grp_info[g] & 0xff) tokens at pool rows grp_row[g] + i (row = page *
+ * page_tokens + slot), attended by the item's local slots
+ * [(info >> 8) & 0xfff, info >> 20).  slot_out per item slot: -1 - leaf
+ * (final output written directly), a partial id, or INT32_MIN (slot unused
+ * by the item).  Arrays stay valid until the next schedule call. */
 typedef struct ta_schedule_view {
-    int32_t n_units;
-    const int32_t* unit_kind;
-    const int32_t* unit_desc;   /* [n_units][4]: tok_begin, n_tokens, slot_begin, n_slots */
-    const int32_t* tok_row;
-    const uint32_t* tok_be;
+    int32_t n_ctas;
+    const int32_t* cta_begin;   /* [n_ctas + 1] */
+    int32_t n_items;
+    const int32_t* items;
+    int32_t n_tiles;
+    const int32_t* tiles;
+    int32_t n_grp;
+    const int32_t* grp_row;
+    const uint32_t* grp_info;
+    int32_t n_slot_leaf;
     const int32_t* slot_leaf;   /* leaf index in leaves() order */
-    const int32_t* slot_part;
+    int32_t n_slot_out;
+    const int32_t* slot_out;
+    int32_t n_partials;
+    const int32_t* part_merge;  /* partial id -> merge record */
     int32_t n_merge;
     const int32_t* merge_leaf;
-    const int32_t* merge_begin; /* [n_merge+1] */
+    const int32_t* merge_head;
+    const int32_t* merge_begin; /* [n_merge + 1] */
     const int32_t* merge_parts;
-    int32_t n_partials;
+    int32_t n_empty;
+    const int32_t* empty;       /* [n_empty][2] (leaf, local kv head) */
+    int32_t n_lanes;
+    int32_t use_mma;
 } ta_schedule_view;
 ta_status ta_schedule_get(ta_ctx* ctx, int block_size, ta_schedule_view* out);
 

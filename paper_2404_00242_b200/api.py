@@ -218,22 +218,29 @@ class TreeAttention:
         return IoStats(**{f: getattr(s, f) for f, _ in capi.IoStats._fields_})
 
     def schedule(self, block_size: int = 128) -> dict:
-        """The device schedule (units, per-token rows/masks, merge lists) as numpy arrays."""
+        """The device schedule (see include/treeattn_b200.h, ta_schedule_view)
+        as numpy arrays: items [n][8], tiles [n][4] (+ decoded ng / boxes),
+        groups, slot maps, partial/merge lists, empty leaf-heads."""
         v = capi.ScheduleView()
         check(lib().ta_schedule_get(self._h, int(block_size), C.byref(v)), "schedule")
 
-        def arr(p, n, dt):
+        def arr(p, n, dt=np.int64):
             return np.ctypeslib.as_array(p, shape=(n,)).astype(dt) if n else np.zeros(0, dt)
-        desc = arr(v.unit_desc, 4 * v.n_units, np.int64).reshape(-1, 4)
-        n_tok = int(desc[:, 0].max() + desc[desc[:, 0].argmax(), 1]) if v.n_units else 0
-        n_slot = int((desc[:, 2] + desc[:, 3]).max()) if v.n_units else 0
+        tiles = arr(v.tiles, 4 * v.n_tiles).reshape(-1, 4)
+        raw = tiles.astype(np.int32).view(np.uint8).reshape(-1, 16) if v.n_tiles else np.zeros((0, 16), np.uint8)
         n_mp = v.merge_begin[v.n_merge] if v.n_merge else 0
-        return {"kind": arr(v.unit_kind, v.n_units, np.int64), "desc": desc,
-                "tok_row": arr(v.tok_row, n_tok, np.int64), "tok_be": arr(v.tok_be, n_tok, np.int64),
-                "slot_leaf": arr(v.slot_leaf, n_slot, np.int64), "slot_part": arr(v.slot_part, n_slot, np.int64),
-                "merge_leaf": arr(v.merge_leaf, v.n_merge, np.int64),
-                "merge_begin": arr(v.merge_begin, v.n_merge + 1, np.int64),
-                "merge_parts": arr(v.merge_parts, n_mp, np.int64), "n_partials": v.n_partials}
+        return {"n_ctas": v.n_ctas, "cta_begin": arr(v.cta_begin, v.n_ctas + 1),
+                "items": arr(v.items, 8 * v.n_items).reshape(-1, 8),
+                "tile_grp_begin": tiles[:, 0] if v.n_tiles else np.zeros(0, np.int64),
+                "tile_ng": raw[:, 4].astype(np.int64), "tile_nbox": raw[:, 5].astype(np.int64),
+                "tile_boxes": raw[:, 8:16].astype(np.int64),
+                "grp_row": arr(v.grp_row, v.n_grp), "grp_info": arr(v.grp_info, v.n_grp),
+                "slot_leaf": arr(v.slot_leaf, v.n_slot_leaf), "slot_out": arr(v.slot_out, v.n_slot_out),
+                "n_partials": v.n_partials, "part_merge": arr(v.part_merge, v.n_partials),
+                "merge_leaf": arr(v.merge_leaf, v.n_merge), "merge_head": arr(v.merge_head, v.n_merge),
+                "merge_begin": arr(v.merge_begin, v.n_merge + 1), "merge_parts": arr(v.merge_parts, n_mp),
+                "empty": arr(v.empty, 2 * v.n_empty).reshape(-1, 2), "n_lanes": v.n_lanes,
+                "use_mma": bool(v.use_mma)}
 
     def launches_per_attend(self) -> int:
         return lib().ta_launches_per_attend(self._h)

@@ -89,12 +89,18 @@ class IoStats(C.Structure):
 
 
 class ScheduleView(C.Structure):
-    _fields_ = [("n_units", C.c_int32), ("unit_kind", C.POINTER(C.c_int32)), ("unit_desc", C.POINTER(C.c_int32)),
-                ("tok_row", C.POINTER(C.c_int32)), ("tok_be", C.POINTER(C.c_uint32)),
-                ("slot_leaf", C.POINTER(C.c_int32)), ("slot_part", C.POINTER(C.c_int32)),
+    _fields_ = [("n_ctas", C.c_int32), ("cta_begin", C.POINTER(C.c_int32)),
+                ("n_items", C.c_int32), ("items", C.POINTER(C.c_int32)),
+                ("n_tiles", C.c_int32), ("tiles", C.POINTER(C.c_int32)),
+                ("n_grp", C.c_int32), ("grp_row", C.POINTER(C.c_int32)), ("grp_info", C.POINTER(C.c_uint32)),
+                ("n_slot_leaf", C.c_int32), ("slot_leaf", C.POINTER(C.c_int32)),
+                ("n_slot_out", C.c_int32), ("slot_out", C.POINTER(C.c_int32)),
+                ("n_partials", C.c_int32), ("part_merge", C.POINTER(C.c_int32)),
                 ("n_merge", C.c_int32), ("merge_leaf", C.POINTER(C.c_int32)),
-                ("merge_begin", C.POINTER(C.c_int32)), ("merge_parts", C.POINTER(C.c_int32)),
-                ("n_partials", C.c_int32)]
+                ("merge_head", C.POINTER(C.c_int32)), ("merge_begin", C.POINTER(C.c_int32)),
+                ("merge_parts", C.POINTER(C.c_int32)),
+                ("n_empty", C.c_int32), ("empty", C.POINTER(C.c_int32)),
+                ("n_lanes", C.c_int32), ("use_mma", C.c_int32)]
 
 
 _lib = None

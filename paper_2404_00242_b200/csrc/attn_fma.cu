@@ -1,57 +1,40 @@
-// attn_fma.cu -- FMA path of the chunk attention (sparse chunks, fp32 KV),
-// the split-K (m, l, O) merge, and the KV scatter used by ta_kv_write.
+// attn_fma.cu -- persistent warp-FMA chunk attention (fp32 or bf16 KV, any
+// supported D, <= 8 or 16 rows per lane) and the KV scatter of ta_kv_write.
 //
-// Reference semantics: group_attention (attention.hpp:117-204) computes, per
-// query and head, an online softmax over the group's tokens whose mask bit
-// is set; tree_reduce (attention.hpp:209-233) merges a query's partials by
-// LSE weighting.  Here one CTA runs a whole unit (a span of consecutive
-// flatten chunks for a block of query slots and one kv head): the KV rows
-// are staged in shared memory once with cp.async (double-buffered tiles of
-// TT tokens), and every (slot, q-head) row that shares the tile consumes
-// them.  The mask is the slot range [b, e) per token (a contiguous run, as
-// every reference mask word is).  Each warp owns TT/8 tokens of every tile
-// and keeps its own running (m, l, O) for all rows; warps are merged once at
-// the end of the unit, so nothing leaves the SM per chunk.
-#include <cuda_bf16.h>
-
+// Same schedule as the tcgen05 kernel (items of tiles of 16-row groups, see
+// ta_internal.h), for sparse lanes and for dtypes / head dims the tensor-core
+// path does not take.  A CTA (8 warps) stages each tile's K/V rows in SMEM
+// once (cp.async, 2 stages); warp w owns tokens [w*TPW, (w+1)*TPW) of every
+// tile (in sub-batches of SB = 64/R tokens) and keeps its own running
+// (m, l, O) for all rows of the item:
+//   QK   lane owns D/32 dims; the SB x R partial dot products are reduced
+//        across the warp by a butterfly transpose-reduction (one shuffle per
+//        dot product), leaving each lane with whole scores
+//   mask token >= group count, or row's slot outside the group's [b, e)
+//   P    exp2 online softmax; P goes through a per-warp SMEM buffer and is
+//        read back as broadcasts for O += P V (lane owns D/32 dims)
+// The warps' states are merged once per item, then written as the final
+// output or a partial with the same last-arriver merge as the MMA kernel.
+//
+// Reference semantics: group_attention (attention.hpp:117-204) and
+// tree_reduce (attention.hpp:209-233).
+#include <algorithm>
 #include <cfloat>
-#include <cmath>
 
-#include "ta_kernels.h"
+#include "ta_ptx.cuh"
 
 namespace ta {
 namespace {
 
-constexpr float kLn2 = 0.69314718055994530942f;
+using namespace dev;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+__device__ __forceinline__ void cp_async16(uint32_t s, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-__device__ __forceinline__ float to_f(float x) { return x; }
-__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
-
-__device__ __forceinline__ void load8(const float* p, float (&f)[8]) {
-    const float4 a = reinterpret_cast<const float4*>(p)[0];
-    const float4 b = reinterpret_cast<const float4*>(p)[1];
-    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
-    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-}
-__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
-    const uint4 u = *reinterpret_cast<const uint4*>(p);
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float2 x = __bfloat1622float2(h[i]);
-        f[2 * i] = x.x;
-        f[2 * i + 1] = x.y;
-    }
 }
 
 template <int N>
@@ -63,8 +46,7 @@ __device__ __forceinline__ void loadN(const float* p, float (&f)[N]) {
         const float2 a = *reinterpret_cast<const float2*>(p);
         f[0] = a.x; f[1] = a.y;
     } else {
-#pragma unroll
-        for (int i = 0; i < N; ++i) f[i] = p[i];
+        f[0] = p[0];
     }
 }
 template <int N>
@@ -78,390 +60,359 @@ __device__ __forceinline__ void loadN(const __nv_bfloat16* p, float (&f)[N]) {
         const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
         f[0] = a.x; f[1] = a.y;
     } else {
-#pragma unroll
-        for (int i = 0; i < N; ++i) f[i] = __bfloat162float(p[i]);
+        f[0] = __bfloat162float(p[0]);
     }
-}
-
-__device__ __forceinline__ void store_out(void* out, size_t idx, float v, int bf16) {
-    if (bf16)
-        reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
-    else
-        reinterpret_cast<float*>(out)[idx] = v;
 }
 
 template <typename T, int D>
 struct FmaCfg {
     static constexpr int NW = 8;
-    static constexpr int TT_RAW = 65536 / (2 * D * (int)sizeof(T));
-    static constexpr int TT = TT_RAW < 512 ? TT_RAW : 512;   // tokens per tile
-    static constexpr int TPW = TT / NW;                       // tokens per warp
-    static constexpr int DQ = D < 32 ? D : 32;                // dims per lane (QK)
-    static constexpr int LPT = D / DQ;                        // lanes per token
-    static constexpr int NT = TPW * LPT / 32;                 // tokens per lane
-    static constexpr int ROWE = D + 16 / (int)sizeof(T);      // padded smem row
-    static constexpr int DPL = D >= 32 ? D / 32 : 1;          // dims per lane (PV)
-    static constexpr int PVL = D / DPL;                       // active PV lanes
+    static constexpr int TG0 = 32768 / (16 * D * (int)sizeof(T));
+    static constexpr int TG = TG0 < 8 ? TG0 : 8;              // groups per tile (= fma_tile_groups)
+    static constexpr int TROWS = 16 * TG;                     // rows per tile stage
+    static constexpr int TPW = TROWS / NW;                    // tokens per warp per tile
+    static constexpr int DPL = D >= 32 ? D / 32 : 1;          // dims per lane
     static constexpr int CPR = D * (int)sizeof(T) / 16;       // 16-byte chunks per row
-    static_assert(NT >= 1 && TPW * LPT % 32 == 0, "tile shape");
-    static_assert(DQ % 8 == 0, "D must be a multiple of 8");
+    static_assert(TG >= 1 && TPW >= 1, "tile shape");
 };
 
 template <typename T, int D, int R>
 constexpr size_t fma_smem_bytes() {
     using C = FmaCfg<T, D>;
-    size_t kv = 2ull * 2 * C::TT * C::ROWE * sizeof(T);
-    size_t be = 2ull * C::TT * 4;
-    size_t qs = (size_t)R * C::LPT * (C::DQ + 4) * 4;
-    size_t pb = (size_t)C::NW * C::TPW * R * 4;
-    size_t comb = (size_t)C::NW * R * (D + 2) * 4;
-    size_t a = kv + be + qs + pb;
-    return a > comb ? a : comb;
+    return 2ull * 2 * C::TROWS * D * sizeof(T)            // K, V stages
+           + (size_t)C::NW * 64 * 4                       // P buffers (64 per warp)
+           + (size_t)C::NW * R * (D + 2) * 4;             // warp combine
 }
 
 template <typename T, int D, int R>
 __global__ void __launch_bounds__(256, 1) attn_fma_kernel(const AttnArgs a) {
     using C = FmaCfg<T, D>;
-    constexpr int TT = C::TT, TPW = C::TPW, DQ = C::DQ, LPT = C::LPT, NT = C::NT, ROWE = C::ROWE;
-    constexpr int DPL = C::DPL, CPR = C::CPR, EPC = 16 / (int)sizeof(T);
+    constexpr int NW = C::NW, TROWS = C::TROWS, TPW = C::TPW, DPL = C::DPL, CPR = C::CPR;
+    constexpr int SB = 64 / R < TPW ? 64 / R : TPW;   // tokens per sub-batch (64 dot products)
+    static_assert(TPW % SB == 0, "sub-batches");
+    constexpr int NV = SB * R;                  // partial dots per lane before the reduction
+    constexpr int VPL = NV / 32;                // whole scores per lane after it
+    static_assert(NV % 32 == 0 && VPL >= 1, "SB * R must be a multiple of 32");
+    static_assert(R % VPL == 0, "rows per lane");
+    constexpr int RCLS = R / VPL;               // lanes l, l + RCLS, ... hold the same rows
     extern __shared__ __align__(16) uint8_t smem[];
     T* Ks = reinterpret_cast<T*>(smem);
-    T* Vs = Ks + 2 * TT * ROWE;
-    uint32_t* be_s = reinterpret_cast<uint32_t*>(Vs + 2 * TT * ROWE);
-    float* qs = reinterpret_cast<float*>(be_s + 2 * TT);
-    float* pbuf = qs + R * LPT * (DQ + 4);
+    T* Vs = Ks + 2 * TROWS * D;
+    float* pbuf = reinterpret_cast<float*>(Vs + 2 * TROWS * D);
+    float* acc_s = pbuf + NW * 64;
+    float* m_s = acc_s + NW * R * D;
+    float* l_s = m_s + NW * R;
 
-    const int kvh = blockIdx.y;
-    const UnitDesc U = a.units[blockIdx.x];
-    const int G = a.G;
-    const int nrows = U.n_slots * G;
-    const T* kb = reinterpret_cast<const T*>(a.k) + (size_t)kvh * a.head_stride;
-    const T* vb = reinterpret_cast<const T*>(a.v) + (size_t)kvh * a.head_stride;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int it0 = a.cta_begin[blockIdx.x], it1 = a.cta_begin[blockIdx.x + 1];
+    const int G = a.G;
+    pdl_launch_dependents();
+    pdl_wait();
+    if (warp == NW - 1) fill_empty(a, lane);
+    if (it0 == it1) return;
 
-    // queries of the unit's rows, pre-scaled by log2(e)/sqrt(D)
-    for (int i = tid; i < R * D; i += 256) {
-        const int r = i / D, d = i % D;
-        float v = 0.f;
-        if (r < nrows) {
-            const int leaf = a.slot_leaf[U.slot_begin + r / G];
-            const int hq = kvh * G + r % G;
-            v = to_f(reinterpret_cast<const T*>(a.q)[((size_t)leaf * a.hq_loc + hq) * D + d]) * a.scale_log2;
+    // cp.async of one tile's K/V rows into stage st
+    auto issue = [&](int ii, int t, int st) {
+        const ItemDesc I = a.items[ii];
+        const TileDesc td = a.tiles[t];
+        const T* kb = reinterpret_cast<const T*>(a.k) + (size_t)I.head * a.head_stride;
+        const T* vb = reinterpret_cast<const T*>(a.v) + (size_t)I.head * a.head_stride;
+        const uint32_t ks = smem_u32(Ks + st * TROWS * D), vs = smem_u32(Vs + st * TROWS * D);
+        for (int c = tid; c < td.ng * 16 * CPR; c += 256) {
+            const int rr = c / CPR, ch = c % CPR;
+            const uint32_t info = a.grp_info[td.grp_begin + (rr >> 4)];
+            if ((rr & 15) >= (int)(info & 0xffu)) continue;
+            const size_t g = ((size_t)a.grp_row[td.grp_begin + (rr >> 4)] + (rr & 15)) * D;
+            cp_async16(ks + (uint32_t)(rr * D * sizeof(T) + ch * 16), reinterpret_cast<const uint8_t*>(kb + g) + ch * 16);
+            cp_async16(vs + (uint32_t)(rr * D * sizeof(T) + ch * 16), reinterpret_cast<const uint8_t*>(vb + g) + ch * 16);
         }
-        qs[(r * LPT + d / DQ) * (DQ + 4) + d % DQ] = v;
-    }
-
-    auto issue = [&](int tile, int st) {
-        const int t0 = tile * TT;
-        const int nv = min(TT, U.n_tokens - t0);
-        const int32_t* rows = a.tok_row + U.tok_begin + t0;
-        for (int c = tid; c < nv * CPR; c += 256) {
-            const int row = c / CPR, ch = c % CPR;
-            const size_t g = (size_t)rows[row] * D + ch * EPC;
-            cp_async16(Ks + (st * TT + row) * ROWE + ch * EPC, kb + g);
-            cp_async16(Vs + (st * TT + row) * ROWE + ch * EPC, vb + g);
-        }
-        for (int t = tid; t < TT; t += 256) be_s[st * TT + t] = t < nv ? a.tok_be[U.tok_begin + t0 + t] : 0u;
         cp_async_commit();
     };
+    // (item, tile) cursor of the next tile to stage (runs ahead across items)
+    int nx_i = it0, nx_t = a.items[it0].tile_begin;
+    auto advance = [&]() {
+        if (++nx_t >= a.items[nx_i].tile_end && ++nx_i < it1) nx_t = a.items[nx_i].tile_begin;
+    };
+    issue(nx_i, nx_t, 0);
+    advance();
+    int gt = 0;
 
-    float m[R], l[R], acc[R][DPL];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        m[r] = -INFINITY;
-        l[r] = 0.f;
-#pragma unroll
-        for (int i = 0; i < DPL; ++i) acc[r][i] = 0.f;
-    }
-
-    const int tl = lane / LPT, part = lane % LPT;
-    const int ntiles = (U.n_tokens + TT - 1) / TT;
-    issue(0, 0);
-    for (int it = 0; it < ntiles; ++it) {
-        const int st = it & 1;
-        if (it + 1 < ntiles) {
-            issue(it + 1, st ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const int nv = min(TT, U.n_tokens - it * TT);
-        const T* Kst = Ks + st * TT * ROWE;
-        const T* Vst = Vs + st * TT * ROWE;
-        const uint32_t* bes = be_s + st * TT;
-
-        // ---- scores: lane group (tl) owns NT tokens, LPT lanes split D
-        float s[NT][R];
-#pragma unroll
-        for (int k = 0; k < NT; ++k)
-#pragma unroll
-            for (int r = 0; r < R; ++r) s[k][r] = 0.f;
-#pragma unroll
-        for (int dc = 0; dc < DQ / 8; ++dc) {
-            float kf[NT][8];
-#pragma unroll
-            for (int k = 0; k < NT; ++k) {
-                const int tok = warp * TPW + tl + k * (32 / LPT);
-                load8(Kst + tok * ROWE + part * DQ + dc * 8, kf[k]);
-            }
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                if (r < nrows) {
-                    const float* qp = qs + (r * LPT + part) * (DQ + 4) + dc * 8;
-                    const float4 qa = *reinterpret_cast<const float4*>(qp);
-                    const float4 qb = *reinterpret_cast<const float4*>(qp + 4);
-#pragma unroll
-                    for (int k = 0; k < NT; ++k)
-                        s[k][r] += kf[k][0] * qa.x + kf[k][1] * qa.y + kf[k][2] * qa.z + kf[k][3] * qa.w +
-                                   kf[k][4] * qb.x + kf[k][5] * qb.y + kf[k][6] * qb.z + kf[k][7] * qb.w;
-                }
-            }
-        }
-#pragma unroll
-        for (int off = 1; off < LPT; off <<= 1)
-#pragma unroll
-            for (int k = 0; k < NT; ++k)
-#pragma unroll
-                for (int r = 0; r < R; ++r) s[k][r] += __shfl_xor_sync(0xffffffffu, s[k][r], off);
-
-        // ---- tree mask: token attended by slots [b, e)
-#pragma unroll
-        for (int k = 0; k < NT; ++k) {
-            const int tok = warp * TPW + tl + k * (32 / LPT);
-            const uint32_t be = bes[tok];
-            const int b = (int)(be & 0xffffu), e = (int)(be >> 16);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int j = r / G;
-                if (j < b || j >= e) s[k][r] = -INFINITY;
-            }
-        }
-
-        // ---- online softmax (base 2), per warp running state
+    for (int ii = it0; ii < it1; ++ii) {
+        const ItemDesc I = a.items[ii];
+        const int nrows = I.n_slots * G;
+        // queries of the item's rows in registers, pre-scaled by log2(e)/sqrt(D)
+        float q[R][DPL];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            if (r < nrows) {
-                float tm = s[0][r];
 #pragma unroll
-                for (int k = 1; k < NT; ++k) tm = fmaxf(tm, s[k][r]);
+            for (int i = 0; i < DPL; ++i) q[r][i] = 0.f;
+            if (r < nrows && lane * DPL < D) {
+                const int leaf = a.slot_leaf[I.slot_begin + r / G];
+                loadN<DPL>(reinterpret_cast<const T*>(a.q) + ((size_t)leaf * a.hq_loc + I.head * G + r % G) * D +
+                               lane * DPL,
+                           q[r]);
 #pragma unroll
-                for (int off = LPT; off < 32; off <<= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, off));
-                if (tm > m[r]) {
-                    const float alpha = exp2f(m[r] - tm);
-                    l[r] *= alpha;
+                for (int i = 0; i < DPL; ++i) q[r][i] *= a.scale_log2;
+            }
+        }
+        float m[R], acc[R][DPL], lsum[VPL];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            m[r] = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < DPL; ++i) acc[r][i] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) lsum[k] = 0.f;
+
+        for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
+            const int st = gt & 1;
+            if (nx_i < it1) {
+                issue(nx_i, nx_t, st ^ 1);
+                advance();
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            const TileDesc td = a.tiles[t];
+            const int grp = (warp * TPW) >> 4, c0 = (warp * TPW) & 15;
+            const uint32_t info = grp < td.ng ? a.grp_info[td.grp_begin + grp] : 0u;
+            const int cnt = max(0, min(TPW, (int)(info & 0xffu) - c0));    // valid tokens of this warp
+            const int b = (int)((info >> 8) & 0xfffu), e = (int)(info >> 20);
+            const T* Kst = Ks + (st * TROWS + warp * TPW) * D;
+            const T* Vst = Vs + (st * TROWS + warp * TPW) * D;
+            for (int sb = 0; sb < cnt; sb += SB) {
+                const int cnt_sb = min(SB, cnt - sb);
+                // ---- partial dots v[tok * R + r] over this lane's dims
+                float v[NV];
+#pragma unroll
+                for (int tk = 0; tk < SB; ++tk) {
+                    float kf[DPL];
+                    if (tk < cnt_sb && lane * DPL < D) {
+                        loadN<DPL>(Kst + (sb + tk) * D + lane * DPL, kf);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < DPL; ++i) kf[i] = 0.f;
+                    }
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        float s = 0.f;
+#pragma unroll
+                        for (int i = 0; i < DPL; ++i) s = fmaf(q[r][i], kf[i], s);
+                        v[tk * R + r] = s;
+                    }
+                }
+                // ---- butterfly transpose-reduction: lane l ends with v[l*VPL .. +VPL)
+#pragma unroll
+                for (int st5 = 0; st5 < 5; ++st5) {
+                    const int off = 16 >> st5, n = NV >> st5;
+                    const bool upper = (lane & off) != 0;
+#pragma unroll
+                    for (int i = 0; i < NV / 2; ++i) {
+                        if (i < n / 2) {
+                            const float send = upper ? v[i] : v[i + n / 2];
+                            const float keep = upper ? v[i + n / 2] : v[i];
+                            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                        }
+                    }
+                }
+                // ---- mask; my values: index l*VPL + k -> (token, row)
+                float mx[VPL];
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    const int idx = lane * VPL + k;
+                    const int tk = idx / R, r = idx % R;
+                    const int jj = r / G;
+                    const bool ok = tk < cnt_sb && r < nrows && jj >= b && jj < e;
+                    v[k] = ok ? v[k] : -INFINITY;
+                    mx[k] = v[k];
+                }
+#pragma unroll
+                for (int off = RCLS; off < 32; off <<= 1)
+#pragma unroll
+                    for (int k = 0; k < VPL; ++k) mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], off));
+                // ---- online softmax: every lane learns every row's new max
+                float alpha_mine[VPL], m_mine[VPL];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float tmx = __shfl_sync(0xffffffffu, mx[r % VPL], r / VPL);
+                    const float nm = fmaxf(m[r], tmx);
+                    const float alpha = (nm == -INFINITY) ? 1.f : ex2(m[r] - nm);
 #pragma unroll
                     for (int i = 0; i < DPL; ++i) acc[r][i] *= alpha;
-                    m[r] = tm;
-                }
-                const bool live = m[r] != -INFINITY;
+                    m[r] = nm;
 #pragma unroll
-                for (int k = 0; k < NT; ++k) {
-                    const float p = live ? exp2f(s[k][r] - m[r]) : 0.f;
-                    if (part == 0) {
-                        l[r] += p;
-                        pbuf[(warp * TPW + tl + k * (32 / LPT)) * R + r] = p;
+                    for (int k = 0; k < VPL; ++k)
+                        if ((lane * VPL + k) % R == r) {
+                            alpha_mine[k] = alpha;
+                            m_mine[k] = nm;
+                        }
+                }
+                float* pw = pbuf + warp * SB * R;
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    const float p = v[k] == -INFINITY ? 0.f : ex2(v[k] - m_mine[k]);
+                    lsum[k] = lsum[k] * alpha_mine[k] + p;
+                    pw[lane * VPL + k] = p;
+                }
+                __syncwarp();
+                // ---- O += P V
+                if (lane * DPL < D) {
+                    for (int tk = 0; tk < cnt_sb; ++tk) {
+                        float vf[DPL];
+                        loadN<DPL>(Vst + (sb + tk) * D + lane * DPL, vf);
+#pragma unroll
+                        for (int r4 = 0; r4 < R; r4 += 4) {
+                            const float4 p4 = *reinterpret_cast<const float4*>(pw + tk * R + r4);
+                            const float pr[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                                for (int i = 0; i < DPL; ++i) acc[r4 + u][i] = fmaf(pr[u], vf[i], acc[r4 + u][i]);
+                        }
                     }
                 }
+                __syncwarp();
             }
+            __syncthreads();   // stage st is refilled by the next issue
         }
-        __syncwarp();
 
-        // ---- O += P V : lane owns DPL output dims
-        const int ntw = min(TPW, nv - warp * TPW);
-        if (lane < C::PVL) {
-            for (int tw = 0; tw < ntw; ++tw) {
-                const int tok = warp * TPW + tw;
-                float vf[DPL];
-                loadN<DPL>(Vst + tok * ROWE + lane * DPL, vf);
-                const float* pp = pbuf + (warp * TPW + tw) * R;
+        // ---- merge the warps' states
 #pragma unroll
-                for (int r4 = 0; r4 < R; r4 += 4) {
-                    if (r4 < nrows) {
-                        const float4 p4 = *reinterpret_cast<const float4*>(pp + r4);
-                        const float pr[4] = {p4.x, p4.y, p4.z, p4.w};
+        for (int k = 0; k < VPL; ++k)
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
+            for (int off = RCLS; off < 32; off <<= 1) lsum[k] += __shfl_xor_sync(0xffffffffu, lsum[k], off);
+        if (lane * DPL < D)
 #pragma unroll
-                            for (int i = 0; i < DPL; ++i) acc[r4 + q][i] += pr[q] * vf[i];
-                    }
-                }
-            }
-        }
-        __syncwarp();
-        __syncthreads();
-    }
-
-    // ---- merge the 8 warps' states, then write partial or final output
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) l[r] += __shfl_xor_sync(0xffffffffu, l[r], off);
-    float* acc_s = reinterpret_cast<float*>(smem);
-    float* m_s = acc_s + C::NW * R * D;
-    float* l_s = m_s + C::NW * R;
-    if (lane < C::PVL) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-            if (r < nrows)
+            for (int r = 0; r < R; ++r)
 #pragma unroll
                 for (int i = 0; i < DPL; ++i) acc_s[(warp * R + r) * D + lane * DPL + i] = acc[r][i];
-    }
-    if (lane == 0) {
+        if (lane < RCLS)
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            m_s[warp * R + r] = m[r];
-            l_s[warp * R + r] = l[r];
-        }
-    }
-    __syncthreads();
-    for (int idx = tid; idx < nrows * D; idx += 256) {
-        const int r = idx / D, d = idx % D;
-        float M = -INFINITY;
+            for (int k = 0; k < VPL; ++k) l_s[warp * R + (lane * VPL + k) % R] = lsum[k];
+        if (lane == 0)
 #pragma unroll
-        for (int w = 0; w < C::NW; ++w) M = fmaxf(M, m_s[w * R + r]);
-        float L = 0.f, O = 0.f;
+            for (int r = 0; r < R; ++r) m_s[warp * R + r] = m[r];
+        __syncthreads();
+        for (int idx = tid; idx < nrows * D; idx += 256) {
+            const int r = idx / D, d = idx % D;
+            const int j = r / G, gq = r % G;
+            const int code = a.slot_out[I.out_begin + j];
+            if (code == kSlotUnused) continue;
+            float M = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < C::NW; ++w) {
-            const float mw = m_s[w * R + r];
-            if (mw != -INFINITY) {
-                const float sc = exp2f(mw - M);
-                L += l_s[w * R + r] * sc;
-                O += acc_s[(w * R + r) * D + d] * sc;
+            for (int w = 0; w < NW; ++w) M = fmaxf(M, m_s[w * R + r]);
+            float L = 0.f, O = 0.f;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const float mw = m_s[w * R + r];
+                if (mw != -INFINITY) {
+                    const float s = ex2(mw - M);
+                    L += l_s[w * R + r] * s;
+                    O += acc_s[(w * R + r) * D + d] * s;
+                }
+            }
+            O = L > 0.f ? O / L : 0.f;
+            const float lse2 = M + log2f(L);
+            const int hq = I.head * G + gq;
+            if (code < 0) {
+                const int leaf = -1 - code;
+                const size_t o = ((size_t)leaf * a.hq_loc + hq) * D + d;
+                if (a.out_bf16)
+                    reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(O);
+                else
+                    reinterpret_cast<float*>(a.out)[o] = O;
+                if (d == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = lse2 * kLn2;
+            } else {
+                a.part_o[((size_t)code * G + gq) * D + d] = O;
+                if (d == 0) a.part_lse[(size_t)code * G + gq] = lse2;
             }
         }
-        O = O / L;
-        const float lse2 = M + log2f(L);
-        const int j = r / G, hq = kvh * G + r % G;
-        const int pid = a.slot_part[U.slot_begin + j];
-        if (pid < 0) {
-            const int leaf = -1 - pid;
-            store_out(a.out, ((size_t)leaf * a.hq_loc + hq) * D + d, O, a.out_bf16);
-            if (d == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = lse2 * kLn2;
-        } else {
-            a.part_o[((size_t)pid * a.hq_loc + hq) * D + d] = O;
-            if (d == 0) a.part_lse[(size_t)pid * a.hq_loc + hq] = lse2;
+        if (I.pad & 1) {
+            // last-arriver merge: one thread per slot takes the ticket
+            __threadfence();
+            __syncthreads();
+            int* flag = reinterpret_cast<int*>(l_s);   // l_s consumed above
+            if (tid < I.n_slots) {
+                const int code = a.slot_out[I.out_begin + tid];
+                int f = 0;
+                if (code >= 0) {
+                    const int mi = a.part_merge[code];
+                    const int need = a.merge_begin[mi + 1] - a.merge_begin[mi];
+                    if (atomicAdd(a.counters + mi, 1) == need - 1) {
+                        a.counters[mi] = 0;   // self-reset for the next launch
+                        f = 1;
+                    }
+                }
+                flag[tid] = f;
+            }
+            __syncthreads();
+            for (int idx = tid; idx < nrows * D; idx += 256) {
+                const int r = idx / D, d = idx % D;
+                const int j = r / G, gq = r % G;
+                if (!flag[j]) continue;
+                __threadfence();
+                const int mi = a.part_merge[a.slot_out[I.out_begin + j]];
+                const int pb = a.merge_begin[mi], pe = a.merge_begin[mi + 1];
+                float M = -INFINITY;
+                for (int p = pb; p < pe; ++p) M = fmaxf(M, __ldcg(a.part_lse + (size_t)a.merge_parts[p] * G + gq));
+                float den = 0.f, O = 0.f;
+                for (int p = pb; p < pe; ++p) {
+                    const int pid = a.merge_parts[p];
+                    const float l2 = __ldcg(a.part_lse + (size_t)pid * G + gq);
+                    if (l2 == -INFINITY) continue;
+                    const float w = ex2(l2 - M);
+                    den += w;
+                    O += w * __ldcg(a.part_o + ((size_t)pid * G + gq) * D + d);
+                }
+                const int leaf = a.merge_leaf[mi], hq = I.head * G + gq;
+                const size_t o = ((size_t)leaf * a.hq_loc + hq) * D + d;
+                const float val = den > 0.f ? O / den : 0.f;
+                if (a.out_bf16)
+                    reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(val);
+                else
+                    reinterpret_cast<float*>(a.out)[o] = val;
+                if (d == 0 && a.lse)
+                    a.lse[(size_t)leaf * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
+            }
         }
+        __syncthreads();   // acc_s / m_s / l_s reuse
     }
 }
 
 template <typename T, int D, int R>
-cudaError_t launch_fma_t(const AttnArgs& a, cudaStream_t s) {
+cudaError_t launch_fma_t(const AttnArgs& a, bool pdl, cudaStream_t s) {
     constexpr size_t smem = fma_smem_bytes<T, D, R>();
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(attn_fma_kernel<T, D, R>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e =
+            cudaFuncSetAttribute(attn_fma_kernel<T, D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    dim3 grid(a.n_units, a.n_kv_loc);
-    attn_fma_kernel<T, D, R><<<grid, 256, smem, s>>>(a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(a.n_ctas);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, attn_fma_kernel<T, D, R>, a);
 }
 
 template <typename T, int R>
-cudaError_t launch_fma_d(const AttnArgs& a, cudaStream_t s) {
+cudaError_t launch_fma_d(const AttnArgs& a, bool pdl, cudaStream_t s) {
     switch (a.D) {
-        case 16: return launch_fma_t<T, 16, R>(a, s);
-        case 32: return launch_fma_t<T, 32, R>(a, s);
-        case 64: return launch_fma_t<T, 64, R>(a, s);
-        case 128: return launch_fma_t<T, 128, R>(a, s);
+        case 16: return launch_fma_t<T, 16, R>(a, pdl, s);
+        case 32: return launch_fma_t<T, 32, R>(a, pdl, s);
+        case 64: return launch_fma_t<T, 64, R>(a, pdl, s);
+        case 128: return launch_fma_t<T, 128, R>(a, pdl, s);
         default: return cudaErrorInvalidValue;
     }
-}
-
-// ---------------------------------------------------------------------------
-// Split-K merge (tree_reduce, attention.hpp:209-233) for leaves covered by
-// more than one unit; partials are consumed in a fixed (unit) order so the
-// result is independent of CTA scheduling.
-template <int DPL>
-__device__ __forceinline__ void load_dpl(const float* p, float (&f)[DPL]) {
-    if constexpr (DPL == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(p);
-        f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
-    } else if constexpr (DPL == 2) {
-        const float2 v = *reinterpret_cast<const float2*>(p);
-        f[0] = v.x; f[1] = v.y;
-    } else {
-        f[0] = p[0];
-    }
-}
-
-// one warp per (merged leaf, q head); lane p fetches partial p's id and lse
-// (all in flight at once), weights are broadcast by shuffle, and the O loads
-// of all partials are independent (no dependent-load chain).  Lane i owns
-// output dims [i*DPL, (i+1)*DPL) (D < 32: lanes >= D idle).
-template <int DPL>
-__global__ void __launch_bounds__(256) merge_kernel(const MergeArgs a) {
-    const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (wid >= a.n_merge * a.hq_loc) return;
-    const int mi = wid / a.hq_loc, hq = wid % a.hq_loc;
-    const int leaf = a.merge_leaf[mi];
-    const int p0 = a.merge_begin[mi], p1 = a.merge_begin[mi + 1];
-    const int D = a.D;
-    const bool active = lane * DPL < D;
-    float acc[DPL];
-#pragma unroll
-    for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
-    float M = -INFINITY, den = 0.f;
-    for (int base = p0; base < p1; base += 32) {
-        const int np = min(32, p1 - base);
-        int pid = 0;
-        float lp = -INFINITY;
-        if (lane < np) {
-            pid = a.merge_parts[base + lane];
-            lp = a.part_lse[(size_t)pid * a.hq_loc + hq];
-        }
-        float bm = lp;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, off));
-        if (bm == -INFINITY) continue;
-        const float nm = fmaxf(M, bm);
-        const float rescale = M == -INFINITY ? 0.f : exp2f(M - nm);
-        den *= rescale;
-#pragma unroll
-        for (int i = 0; i < DPL; ++i) acc[i] *= rescale;
-        M = nm;
-        const float w = lp == -INFINITY ? 0.f : exp2f(lp - M);
-        float ws = w;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, off);
-        den += ws;
-        int p = 0;
-        for (; p + 4 <= np; p += 4) {
-            float v[4][DPL];
-            float wv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int id = __shfl_sync(0xffffffffu, pid, p + u);
-                wv[u] = __shfl_sync(0xffffffffu, w, p + u);
-                if (active) load_dpl<DPL>(a.part_o + ((size_t)id * a.hq_loc + hq) * D + lane * DPL, v[u]);
-            }
-            if (active)
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int i = 0; i < DPL; ++i) acc[i] += wv[u] * v[u][i];
-        }
-        for (; p < np; ++p) {
-            const int id = __shfl_sync(0xffffffffu, pid, p);
-            const float wp = __shfl_sync(0xffffffffu, w, p);
-            if (active) {
-                float v[DPL];
-                load_dpl<DPL>(a.part_o + ((size_t)id * a.hq_loc + hq) * D + lane * DPL, v);
-#pragma unroll
-                for (int i = 0; i < DPL; ++i) acc[i] += wp * v[i];
-            }
-        }
-    }
-    const float inv = den > 0.f ? 1.f / den : 0.f;
-    const size_t base = ((size_t)leaf * a.hq_loc + hq) * D;
-    if (active)
-#pragma unroll
-        for (int i = 0; i < DPL; ++i) store_out(a.out, base + lane * DPL + i, acc[i] * inv, a.out_bf16);
-    if (lane == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
 }
 
 // ---------------------------------------------------------------------------
@@ -485,20 +436,14 @@ __global__ void kv_scatter_kernel(const uint4* __restrict__ sk, const uint4* __r
 
 }  // namespace
 
-cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, cudaStream_t s) {
-    if (a.n_units == 0) return cudaSuccess;
-    if (max_rows <= 8) return a.kv_bf16 ? launch_fma_d<__nv_bfloat16, 8>(a, s) : launch_fma_d<float, 8>(a, s);
-    return a.kv_bf16 ? launch_fma_d<__nv_bfloat16, 16>(a, s) : launch_fma_d<float, 16>(a, s);
+int fma_tile_groups(int D, int esize) {
+    const int tg = 32768 / (16 * D * esize);
+    return tg < 8 ? tg : 8;
 }
 
-cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s) {
-    if (a.n_merge == 0) return cudaSuccess;
-    const int warps = a.n_merge * a.hq_loc;
-    const int blocks = (warps + 7) / 8;
-    if (a.D >= 128) merge_kernel<4><<<blocks, 256, 0, s>>>(a);
-    else if (a.D >= 64) merge_kernel<2><<<blocks, 256, 0, s>>>(a);
-    else merge_kernel<1><<<blocks, 256, 0, s>>>(a);
-    return cudaGetLastError();
+cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, bool pdl, cudaStream_t s) {
+    if (max_rows <= 8) return a.kv_bf16 ? launch_fma_d<__nv_bfloat16, 8>(a, pdl, s) : launch_fma_d<float, 8>(a, pdl, s);
+    return a.kv_bf16 ? launch_fma_d<__nv_bfloat16, 16>(a, pdl, s) : launch_fma_d<float, 16>(a, pdl, s);
 }
 
 cudaError_t launch_kv_scatter(const void* src_k, const void* src_v, void* dst_k, void* dst_v,

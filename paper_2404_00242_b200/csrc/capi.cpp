@@ -51,25 +51,29 @@ struct ta_ctx {
     void* meta_host = nullptr;
     size_t meta_host_cap = 0;
     cudaEvent_t meta_done = nullptr;
-    const UnitDesc* d_units_fma = nullptr;
-    const UnitDesc* d_units_mma = nullptr;
-    const int32_t* d_tok_row = nullptr;
-    const uint32_t* d_tok_be = nullptr;
+    const TileDesc* d_tiles = nullptr;
+    const int32_t* d_grp_row = nullptr;
+    const uint32_t* d_grp_info = nullptr;
+    const ItemDesc* d_items = nullptr;
+    const int32_t* d_cta_begin = nullptr;
     const int32_t* d_slot_leaf = nullptr;
-    const int32_t* d_slot_part = nullptr;
+    const int32_t* d_slot_out = nullptr;
+    const int32_t* d_part_merge = nullptr;
     const int32_t* d_merge_leaf = nullptr;
     const int32_t* d_merge_begin = nullptr;
     const int32_t* d_merge_parts = nullptr;
-    const int32_t* d_grp_row = nullptr;
-    const uint32_t* d_grp_info = nullptr;
+    const int32_t* d_empty = nullptr;
+    bool pdl = true;
+    int num_sms = 148;
 
     // host copy of the schedule for ta_schedule_get
     Schedule dbg_sched;
-    std::vector<int32_t> dbg_kind, dbg_desc;
 
-    // partial scratch
+    // partial scratch + merge counters (self-resetting, zeroed on allocation)
     float* part = nullptr;
     size_t part_cap = 0;  // floats
+    int* counters = nullptr;
+    size_t counters_cap = 0;  // bytes
 
     // staging for kv writes and host-buffer attend
     void* stage_dev = nullptr;
@@ -87,6 +91,7 @@ struct ta_ctx {
             cudaFree(meta_dev);
             cudaFreeHost(meta_host);
             cudaFree(part);
+            cudaFree(counters);
             cudaFree(stage_dev);
             cudaFreeHost(stage_host);
             cudaFree(io_dev);
@@ -203,7 +208,8 @@ ta_status ta_ctx_create(int device, const ta_shape* s, ta_ctx** out) {
             cuda_check(cudaEventCreateWithFlags(&c->meta_done, cudaEventDisableTiming), "cudaEventCreate");
             cudaDeviceProp prop;
             cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-            c->opt.num_sms = prop.multiProcessorCount;
+            c->num_sms = prop.multiProcessorCount;
+            c->opt.num_ctas = prop.multiProcessorCount;
             if (mma_supported(sh.d_head, sh.kv_dtype == TA_BF16)) {
                 const int64_t rows = (int64_t)sh.n_layers * sh.n_local_kv_heads * sh.max_pages * sh.page_tokens;
                 c->tmaps_ok = true;
@@ -232,16 +238,21 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
         } else if (k == "use_mma") {
             c->opt.use_mma = v != 0 && mma_supported(c->shape.d_head, c->shape.kv_dtype == TA_BF16);
         } else if (k == "mma_max_rows") {
-            if (v != 64 && v != 128) fail(TA_ERR_INVALID_ARGUMENT, "mma_max_rows must be 64 or 128");
-            c->opt.mma_max_rows = (int)v;
-        } else if (k == "span_tokens") {
-            c->opt.span_tokens = (int)v;
+            if (v < 1 || v > 128) fail(TA_ERR_INVALID_ARGUMENT, "mma_max_rows must be in [1, 128]");
+            c->opt.max_rows = (int)v;
+        } else if (k == "tile_groups") {
+            if (v < 1 || v > 8) fail(TA_ERR_INVALID_ARGUMENT, "tile_groups must be in [1, 8]");
+            c->opt.tile_groups = (int)v;
+        } else if (k == "tile_cost") {
+            if (v < 0) fail(TA_ERR_INVALID_ARGUMENT, "tile_cost must be >= 0");
+            c->opt.tile_cost = (int)v;
+        } else if (k == "num_ctas") {
+            if (v < 1 || v > 65535) fail(TA_ERR_INVALID_ARGUMENT, "num_ctas must be in [1, 65535]");
+            c->opt.num_ctas = (int)v;
         } else if (k == "final_direct") {
             c->opt.final_direct = v != 0;
-        } else if (k == "trace_ptr") {
-            c->opt.trace_ptr = v;
-        } else if (k == "num_sms") {
-            c->opt.num_sms = (int)v;
+        } else if (k == "pdl") {
+            c->pdl = v != 0;
         } else {
             fail(TA_ERR_INVALID_ARGUMENT, "unknown option " + k);
         }
@@ -418,38 +429,49 @@ ta_status ta_plan_json(ta_ctx* c, int bs, char* buf, size_t cap, size_t* len) {
 }
 
 // ---------------------------------------------------------------- attention
+namespace {
+
+// schedule options as the selected kernel needs them
+SchedOptions effective_opts(const ta_ctx* c) {
+    SchedOptions o = c->opt;
+    o.use_mma = o.use_mma && mma_supported(c->shape.d_head, c->shape.kv_dtype == TA_BF16);
+    if (!o.use_mma) o.tile_groups = fma_tile_groups(c->shape.d_head, c->esize);
+    return o;
+}
+
+}  // namespace
+
 ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
     return guard([&] {
         need_device(c);
         if (c->tree.root < 0) fail(TA_ERR_LOGIC, "no tree");
         cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
-        // always re-plan: one decode step = plan + schedule + attention
+        // one decode step = plan + schedule + metadata upload, reused by every layer
         plan_flatten(c->tree, bs, c->plan);
         c->plan_valid = true;
         c->plan_version = c->tree.version;
         c->plan_bs = bs;
-        build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, c->shape.kv_dtype == TA_BF16,
-                       c->opt, c->sched);
+        const SchedOptions o = effective_opts(c);
+        build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, o, c->sched);
         const Schedule& S = c->sched;
-        if (c->opt.fma_max_rows > 16) fail(TA_ERR_INVALID_ARGUMENT, "fma_max_rows > 16");
-        // pack metadata into one blob
         struct Part {
             const void* src;
             size_t bytes;
             size_t off;
         };
-        Part parts[11] = {
-            {S.units_fma.data(), S.units_fma.size() * sizeof(UnitDesc), 0},
-            {S.units_mma.data(), S.units_mma.size() * sizeof(UnitDesc), 0},
-            {S.tok_row.data(), S.tok_row.size() * 4, 0},
-            {S.tok_be.data(), S.tok_be.size() * 4, 0},
+        Part parts[12] = {
+            {S.tiles.data(), S.tiles.size() * sizeof(TileDesc), 0},
+            {S.grp_row.data(), S.grp_row.size() * 4, 0},
+            {S.grp_info.data(), S.grp_info.size() * 4, 0},
+            {S.items.data(), S.items.size() * sizeof(ItemDesc), 0},
+            {S.cta_begin.data(), S.cta_begin.size() * 4, 0},
             {S.slot_leaf.data(), S.slot_leaf.size() * 4, 0},
-            {S.slot_part.data(), S.slot_part.size() * 4, 0},
+            {S.slot_out.data(), S.slot_out.size() * 4, 0},
+            {S.part_merge.data(), S.part_merge.size() * 4, 0},
             {S.merge_leaf.data(), S.merge_leaf.size() * 4, 0},
             {S.merge_begin.data(), S.merge_begin.size() * 4, 0},
             {S.merge_parts.data(), S.merge_parts.size() * 4, 0},
-            {S.grp_row.data(), S.grp_row.size() * 4, 0},
-            {S.grp_info.data(), S.grp_info.size() * 4, 0},
+            {S.empty.data(), S.empty.size() * 4, 0},
         };
         size_t total = 0;
         for (auto& p : parts) {
@@ -457,7 +479,7 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             total = align_up(total + p.bytes, 256);
         }
         total = std::max<size_t>(total, 256);
-        // previous upload must have consumed the pinned staging
+        // the previous upload must have consumed the pinned staging
         cuda_check(cudaEventSynchronize(c->meta_done), "cudaEventSynchronize");
         grow_host(&c->meta_host, &c->meta_host_cap, total);
         grow_dev(&c->meta_dev, &c->meta_cap, total);
@@ -467,25 +489,35 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         cuda_check(cudaMemcpyAsync(c->meta_dev, c->meta_host, total, cudaMemcpyHostToDevice, s), "metadata upload");
         cuda_check(cudaEventRecord(c->meta_done, s), "cudaEventRecord");
         char* d = (char*)c->meta_dev;
-        c->d_units_fma = (const UnitDesc*)(d + parts[0].off);
-        c->d_units_mma = (const UnitDesc*)(d + parts[1].off);
-        c->d_tok_row = (const int32_t*)(d + parts[2].off);
-        c->d_tok_be = (const uint32_t*)(d + parts[3].off);
-        c->d_slot_leaf = (const int32_t*)(d + parts[4].off);
-        c->d_slot_part = (const int32_t*)(d + parts[5].off);
-        c->d_merge_leaf = (const int32_t*)(d + parts[6].off);
-        c->d_merge_begin = (const int32_t*)(d + parts[7].off);
-        c->d_merge_parts = (const int32_t*)(d + parts[8].off);
-        c->d_grp_row = (const int32_t*)(d + parts[9].off);
-        c->d_grp_info = (const uint32_t*)(d + parts[10].off);
-        // partial scratch: o [n_part][hq][D] + lse [n_part][hq]
-        const size_t pf = (size_t)std::max(1, S.n_partials) * c->hq_loc * (c->shape.d_head + 1);
+        c->d_tiles = (const TileDesc*)(d + parts[0].off);
+        c->d_grp_row = (const int32_t*)(d + parts[1].off);
+        c->d_grp_info = (const uint32_t*)(d + parts[2].off);
+        c->d_items = (const ItemDesc*)(d + parts[3].off);
+        c->d_cta_begin = (const int32_t*)(d + parts[4].off);
+        c->d_slot_leaf = (const int32_t*)(d + parts[5].off);
+        c->d_slot_out = (const int32_t*)(d + parts[6].off);
+        c->d_part_merge = (const int32_t*)(d + parts[7].off);
+        c->d_merge_leaf = (const int32_t*)(d + parts[8].off);
+        c->d_merge_begin = (const int32_t*)(d + parts[9].off);
+        c->d_merge_parts = (const int32_t*)(d + parts[10].off);
+        c->d_empty = (const int32_t*)(d + parts[11].off);
+        // partial scratch: o [n_part][G][D] + lse [n_part][G]
+        const size_t pf = (size_t)std::max(1, S.n_partials) * c->G * (c->shape.d_head + 1);
         if (pf > c->part_cap) {
             void* p = c->part;
             size_t cap = c->part_cap * sizeof(float);
             grow_dev(&p, &cap, pf * sizeof(float));
             c->part = (float*)p;
             c->part_cap = cap / sizeof(float);
+        }
+        const size_t cb = std::max<size_t>(1, S.merge_leaf.size()) * sizeof(int);
+        if (cb > c->counters_cap) {
+            // stream-ordered: earlier launches may still use the old array
+            cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+            void* p = c->counters;
+            grow_dev(&p, &c->counters_cap, cb);
+            c->counters = (int*)p;
+            cuda_check(cudaMemset(c->counters, 0, c->counters_cap), "cudaMemset(counters)");
         }
         c->prepared = true;
         c->prepared_version = c->tree.version;
@@ -503,52 +535,41 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.k = (const char*)c->kv_k + (size_t)layer * c->layer_elems * c->esize;
     a.v = (const char*)c->kv_v + (size_t)layer * c->layer_elems * c->esize;
     a.head_stride = c->head_stride;
-    a.q = q;
-    a.out = out;
-    a.lse = lse;
-    a.part_o = c->part;
-    a.part_lse = c->part + (size_t)std::max(1, S.n_partials) * c->hq_loc * D;
-    a.tok_row = c->d_tok_row;
-    a.tok_be = c->d_tok_be;
-    a.slot_leaf = c->d_slot_leaf;
-    a.slot_part = c->d_slot_part;
-    a.G = c->G;
-    a.hq_loc = c->hq_loc;
-    a.n_kv_loc = c->shape.n_local_kv_heads;
-    a.D = D;
-    a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
-    a.kv_bf16 = c->shape.kv_dtype == TA_BF16;
-    a.out_bf16 = c->shape.out_dtype == TA_BF16;
     a.tmap_k = c->tmap_k;
     a.tmap_v = c->tmap_v;
     a.head_rows = c->shape.max_pages * c->shape.page_tokens;
     a.layer_row0 = (int64_t)layer * c->shape.n_local_kv_heads * a.head_rows;
+    a.q = q;
+    a.out = out;
+    a.lse = lse;
+    a.part_o = c->part;
+    a.part_lse = c->part + (size_t)std::max(1, S.n_partials) * c->G * D;
+    a.counters = c->counters;
+    a.tiles = c->d_tiles;
     a.grp_row = c->d_grp_row;
     a.grp_info = c->d_grp_info;
-    a.trace = reinterpret_cast<long long*>(c->opt.trace_ptr);
-    if (!S.units_fma.empty()) {
-        a.units = c->d_units_fma;
-        a.n_units = (int)S.units_fma.size();
-        cuda_check(launch_attn_fma(a, c->opt.fma_max_rows, s), "attn_fma");
-    }
-    if (!S.units_mma.empty()) {
-        a.units = c->d_units_mma;
-        a.n_units = (int)S.units_mma.size();
-        cuda_check(launch_attn_mma(a, s), "attn_mma");
-    }
-    MergeArgs m{};
-    m.part_o = a.part_o;
-    m.part_lse = a.part_lse;
-    m.merge_leaf = c->d_merge_leaf;
-    m.merge_begin = c->d_merge_begin;
-    m.merge_parts = c->d_merge_parts;
-    m.n_merge = (int)S.merge_leaf.size();
-    m.out = out;
-    m.lse = lse;
-    m.hq_loc = c->hq_loc;
-    m.D = D;
-    m.out_bf16 = a.out_bf16;
-    cuda_check(launch_merge(m, s), "merge");
+    a.items = c->d_items;
+    a.cta_begin = c->d_cta_begin;
+    a.slot_leaf = c->d_slot_leaf;
+    a.slot_out = c->d_slot_out;
+    a.part_merge = c->d_part_merge;
+    a.merge_leaf = c->d_merge_leaf;
+    a.merge_begin = c->d_merge_begin;
+    a.merge_parts = c->d_merge_parts;
+    a.empty = c->d_empty;
+    a.n_empty = (int)(S.empty.size() / 2);
+    a.n_ctas = (int)S.cta_begin.size() - 1;
+    a.G = c->G;
+    a.hq_loc = c->hq_loc;
+    a.D = D;
+    a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+    a.kv_bf16 = c->shape.kv_dtype == TA_BF16;
+    a.out_bf16 = c->shape.out_dtype == TA_BF16;
+    const SchedOptions o = effective_opts(c);
+    if (o.use_mma)
+        cuda_check(launch_attn_mma(a, c->pdl, s), "attn_mma");
+    else
+        cuda_check(launch_attn_fma(a, o.fma_max_rows, c->pdl, s), "attn_fma");
 }
 
 ta_status ta_attend(ta_ctx* c, int layer, const void* q, void* out, float* lse, void* stream) {
@@ -585,18 +606,18 @@ ta_status ta_io_stats_get(ta_ctx* c, ta_io_stats* o) {
         std::memset(o, 0, sizeof(*o));
         o->n_chunks = c->plan.n_chunks();
         o->n_groups = c->plan.n_groups();
-        o->n_units = (int64_t)(S.units_fma.size() + S.units_mma.size());
-        o->n_units_mma = (int64_t)S.units_mma.size();
+        o->n_units = (int64_t)S.items.size();
+        o->n_units_mma = effective_opts(c).use_mma ? (int64_t)S.items.size() : 0;
         o->n_partials = S.n_partials;
         o->kv_bytes = S.kv_tokens_unique * 2 * nl * D * c->esize;
-        o->kv_bytes_loaded = S.kv_tokens_loaded * 2 * nl * D * c->esize;
+        o->kv_bytes_loaded = S.kv_rows_loaded * 2 * D * c->esize;
         o->q_bytes = L * c->hq_loc * D * c->esize;
         o->out_bytes = L * c->hq_loc * D * c->out_esize;
-        o->partial_bytes = (int64_t)S.n_partials * c->hq_loc * (D + 1) * 4 * 2;
-        o->meta_bytes = (int64_t)(S.units_fma.size() + S.units_mma.size()) * sizeof(UnitDesc) +
-                        (int64_t)(S.tok_row.size() + S.tok_be.size() + S.slot_leaf.size() + S.slot_part.size() +
-                                  S.merge_leaf.size() + S.merge_begin.size() + S.merge_parts.size() +
-                                  S.grp_row.size() + S.grp_info.size()) * 4;
+        o->partial_bytes = (int64_t)S.n_partials * c->G * (D + 1) * 4 * 2;
+        o->meta_bytes = (int64_t)(S.tiles.size() * sizeof(TileDesc) + S.items.size() * sizeof(ItemDesc)) +
+                        (int64_t)(S.grp_row.size() + S.grp_info.size() + S.cta_begin.size() + S.slot_leaf.size() +
+                                  S.slot_out.size() + S.part_merge.size() + S.merge_leaf.size() +
+                                  S.merge_begin.size() + S.merge_parts.size() + S.empty.size()) * 4;
         o->flops = S.masked_q_tokens * c->hq_loc * 4 * D;
     });
 }
@@ -606,34 +627,38 @@ ta_status ta_schedule_get(ta_ctx* c, int bs, ta_schedule_view* o) {
         if (c->tree.root < 0) fail(TA_ERR_LOGIC, "no tree");
         ensure_plan(c, bs);
         Schedule& S = c->dbg_sched;
-        build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, c->shape.kv_dtype == TA_BF16,
-                       c->opt, S);
-        c->dbg_kind.clear();
-        c->dbg_desc.clear();
-        for (int k = 0; k < 2; ++k)
-            for (const UnitDesc& u : k ? S.units_mma : S.units_fma) {
-                c->dbg_kind.push_back(k);
-                c->dbg_desc.insert(c->dbg_desc.end(), {u.tok_begin, u.n_tokens, u.slot_begin, u.n_slots});
-            }
-        o->n_units = (int32_t)c->dbg_kind.size();
-        o->unit_kind = c->dbg_kind.data();
-        o->unit_desc = c->dbg_desc.data();
-        o->tok_row = S.tok_row.data();
-        o->tok_be = S.tok_be.data();
+        build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, effective_opts(c), S);
+        std::memset(o, 0, sizeof(*o));
+        o->n_ctas = (int32_t)S.cta_begin.size() - 1;
+        o->cta_begin = S.cta_begin.data();
+        o->n_items = (int32_t)S.items.size();
+        o->items = reinterpret_cast<const int32_t*>(S.items.data());
+        o->n_tiles = (int32_t)S.tiles.size();
+        o->tiles = reinterpret_cast<const int32_t*>(S.tiles.data());
+        o->n_grp = (int32_t)S.grp_row.size();
+        o->grp_row = S.grp_row.data();
+        o->grp_info = S.grp_info.data();
+        o->n_slot_leaf = (int32_t)S.slot_leaf.size();
         o->slot_leaf = S.slot_leaf.data();
-        o->slot_part = S.slot_part.data();
+        o->n_slot_out = (int32_t)S.slot_out.size();
+        o->slot_out = S.slot_out.data();
+        o->n_partials = S.n_partials;
+        o->part_merge = S.part_merge.data();
         o->n_merge = (int32_t)S.merge_leaf.size();
         o->merge_leaf = S.merge_leaf.data();
+        o->merge_head = S.merge_head.data();
         o->merge_begin = S.merge_begin.data();
         o->merge_parts = S.merge_parts.data();
-        o->n_partials = S.n_partials;
+        o->n_empty = (int32_t)(S.empty.size() / 2);
+        o->empty = S.empty.data();
+        o->n_lanes = S.n_lanes;
+        o->use_mma = effective_opts(c).use_mma ? 1 : 0;
     });
 }
 
 int ta_launches_per_attend(ta_ctx* c) {
     if (!c || !c->prepared) return 0;
-    return (c->sched.units_fma.empty() ? 0 : 1) + (c->sched.units_mma.empty() ? 0 : 1) +
-           (c->sched.merge_leaf.empty() ? 0 : 1);
+    return 1;
 }
 
 }  // extern "C"

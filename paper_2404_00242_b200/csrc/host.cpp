@@ -411,209 +411,267 @@ std::string plan_json(const Tree& t, const Plan& p) {
 }
 
 // ===========================================================================
-// Device schedule.
+// Device schedule (see ta_internal.h for the vocabulary).
 //
-// Every flatten chunk is one unit of KV streaming work.  Its query list is
-// cut into blocks of at most S slots (S = rows-per-unit / G, rows being
-// (query, q-head-in-group) pairs); a block keeps only the segments some of
-// its queries attend.  Consecutive chunks whose blocks fit together are
-// merged into one unit (a span), so queries that persist across chunks
-// (shared prefixes) accumulate on-chip and leave one (m, l, O) partial per
-// span instead of one per chunk.  Leaves covered by a single unit are
-// written directly; the rest are merged by the merge kernel in unit order.
+// 1. Stripes.  Walk the flatten chunks in order.  A chunk whose query set fits
+//    a row tile (|Q| <= S = max_rows / G slots) joins the open stripe while
+//    the union of query sets still fits; a wider chunk joins an open wide
+//    stripe with the identical query set.  Queries that persist across chunks
+//    (shared prefixes, long branches) therefore accumulate on chip.
+// 2. Lanes.  A stripe with |Q| slots is cut into ceil(|Q| / S) balanced slot
+//    blocks; each block streams only the stripe tokens its slots attend, as
+//    16-row groups (consecutive pool rows, one slot range) and 8-group tiles.
+//    The blocks of a wide stripe read the same KV; they are adjacent in the
+//    sequence so they run concurrently and the repeat reads hit L2.
+// 3. CTA runs.  The sequence (head, lane, tile) is cut into num_ctas
+//    contiguous runs of equal cost (box rows + a fixed per-tile cost); each
+//    run's maximal (head, lane) pieces are its items.
+// 4. Outputs.  A leaf-head attended by one item is written directly; else
+//    every item writes a partial and the last one to finish merges them in
+//    item order (tree_reduce, attention.hpp:209-233).
 // ===========================================================================
 namespace {
 
-struct Piece {
-    int32_t node;
-    int64_t off, len;
-    int32_t lo, hi;
+struct Stripe {
+    int c0 = 0, c1 = 0;             // chunk range [c0, c1) (chunks with no queries skipped inside)
+    std::vector<int32_t> qset;      // sorted leaf indices
+    bool wide = false;
 };
 
-constexpr int kMaxUnitGroups = 256;  // = MAX_GRP of attn_mma.cu
-
-struct OpenUnit {
-    std::vector<int32_t> slots;  // sorted leaf indices
-    std::vector<Piece> pieces;
-    int64_t tokens = 0;
-    int64_t grp_est = 0;         // upper bound on 16-row TMA groups
-    int last_chunk = -1;
-    bool mma = false;
+struct Lane {
+    int32_t slot_begin = 0, n_slots = 0;
+    int32_t tile_begin = 0, tile_end = 0;
 };
-
-void sorted_union(const std::vector<int32_t>& a, const int32_t* b, int nb, std::vector<int32_t>& out) {
-    out.clear();
-    std::set_union(a.begin(), a.end(), b, b + nb, std::back_inserter(out));
-}
 
 }  // namespace
 
-void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G,
-                    int n_kv_heads_local, bool bf16, const SchedOptions& opt, Schedule& S) {
+void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G, int n_heads,
+                    const SchedOptions& opt, Schedule& S) {
     S = Schedule{};
     S.n_leaves = (int32_t)t.leaves.size();
     const int P = pool.page_size;
     const int nc = plan.n_chunks();
+    const int max_rows = opt.use_mma ? opt.max_rows : opt.fma_max_rows;
+    const int S_max = std::max(1, max_rows / std::max(1, G));
+    const int TG = std::clamp(opt.tile_groups, 1, 8);
+    if (S_max > 4095) fail(TA_ERR_INVALID_ARGUMENT, "schedule: too many slots per lane");
 
-    // --- per-chunk path and query blocks
-    struct Block {
-        int chunk;
-        int q0, q1;  // into plan.chunk_q
-        bool mma;
-        int64_t tokens;
-        int64_t grp_est;
-    };
-    std::vector<Block> blocks;
-    int64_t work_tokens = 0;
+    // ---- 1. stripes
+    std::vector<Stripe> stripes;
+    std::vector<int32_t> tmp;
     for (int c = 0; c < nc; ++c) {
         const int qb = plan.chunk_q_begin[c], qe = plan.chunk_q_begin[c + 1];
         const int nq = qe - qb;
-        if (nq == 0) continue;
-        const int64_t rows = (int64_t)nq * G;
-        const bool mma = bf16 && opt.use_mma && rows > opt.fma_max_rows;
-        const int cap_rows = mma ? opt.mma_max_rows : opt.fma_max_rows;
-        const int S_slots = std::max(1, cap_rows / G);
-        const int nb = (nq + S_slots - 1) / S_slots;
-        for (int k = 0; k < nb; ++k) {
-            const int a = qb + (int)((int64_t)nq * k / nb);
-            const int b = qb + (int)((int64_t)nq * (k + 1) / nb);
-            int64_t toks = 0, grp = 0;
-            for (int s = plan.chunk_seg_begin[c]; s < plan.chunk_seg_begin[c + 1]; ++s)
-                if (plan.cseg_hi[s] > plan.chunk_q[a] && plan.cseg_lo[s] <= plan.chunk_q[b - 1]) {
-                    toks += plan.cseg_len[s];
-                    grp += (plan.cseg_len[s] + 15) / 16 + 1;
-                }
-            blocks.push_back({c, a, b, mma, toks, grp});
-            work_tokens += toks;
-        }
         for (int s = plan.chunk_seg_begin[c]; s < plan.chunk_seg_begin[c + 1]; ++s)
             S.kv_tokens_unique += plan.cseg_len[s];
+        if (nq == 0) continue;
+        const int32_t* q = plan.chunk_q.data() + qb;
+        Stripe* cur = stripes.empty() ? nullptr : &stripes.back();
+        if (nq > S_max) {
+            if (cur && cur->wide && (int)cur->qset.size() == nq && std::equal(q, q + nq, cur->qset.begin())) {
+                cur->c1 = c + 1;
+                continue;
+            }
+            stripes.push_back({c, c + 1, std::vector<int32_t>(q, q + nq), true});
+            continue;
+        }
+        if (cur && !cur->wide) {
+            tmp.clear();
+            std::set_union(cur->qset.begin(), cur->qset.end(), q, q + nq, std::back_inserter(tmp));
+            if ((int)tmp.size() <= S_max) {
+                cur->qset.swap(tmp);
+                cur->c1 = c + 1;
+                continue;
+            }
+        }
+        stripes.push_back({c, c + 1, std::vector<int32_t>(q, q + nq), false});
+    }
+    S.n_stripes = (int64_t)stripes.size();
+
+    // ---- 2. lanes: groups and tiles
+    std::vector<Lane> lanes;
+    for (const Stripe& st : stripes) {
+        const int nq = (int)st.qset.size();
+        const int nb = (nq + S_max - 1) / S_max;
+        for (int k = 0; k < nb; ++k) {
+            Lane ln;
+            const int a = (int)((int64_t)nq * k / nb), b = (int)((int64_t)nq * (k + 1) / nb);
+            ln.slot_begin = (int32_t)S.slot_leaf.size();
+            ln.n_slots = b - a;
+            S.slot_leaf.insert(S.slot_leaf.end(), st.qset.begin() + a, st.qset.begin() + b);
+            const int32_t* sl = S.slot_leaf.data() + ln.slot_begin;
+            ln.tile_begin = (int32_t)S.tiles.size();
+            int32_t g_open = -1;        // open group (may take more tokens)
+            int32_t tile_g0 = (int32_t)S.grp_row.size();
+            auto close_tile = [&](bool force) {
+                const int32_t ng = (int32_t)S.grp_row.size() - tile_g0;
+                if (ng == 0 || (!force && ng < TG)) return;
+                TileDesc td{};
+                td.grp_begin = tile_g0;
+                td.ng = (uint8_t)ng;
+                int ntok = 0;
+                for (int g = 0; g < ng; ++g) ntok += (int)(S.grp_info[tile_g0 + g] & 0xffu);
+                td.ntok = (uint16_t)ntok;
+                // TMA boxes: runs of full, row-contiguous groups as 8/4/2/1-group boxes
+                int nbx = 0, g = 0;
+                while (g < ng) {
+                    int run = 1;
+                    while (g + run < ng && (S.grp_info[tile_g0 + g + run - 1] & 0xffu) == 16u &&
+                           S.grp_row[tile_g0 + g + run] == S.grp_row[tile_g0 + g] + 16 * run)
+                        ++run;
+                    while (run > 0) {
+                        int sz = 3;
+                        while ((1 << sz) > run) --sz;
+                        td.box[nbx++] = (uint8_t)((g << 2) | sz);
+                        g += 1 << sz;
+                        run -= 1 << sz;
+                    }
+                }
+                td.nbox = (uint8_t)nbx;
+                S.tiles.push_back(td);
+                tile_g0 = (int32_t)S.grp_row.size();
+                g_open = -1;
+            };
+            for (int c = st.c0; c < st.c1; ++c) {
+                for (int s = plan.chunk_seg_begin[c]; s < plan.chunk_seg_begin[c + 1]; ++s) {
+                    const int32_t lo = plan.cseg_lo[s], hi = plan.cseg_hi[s];
+                    const int bb = (int)(std::lower_bound(sl, sl + ln.n_slots, lo) - sl);
+                    const int ee = (int)(std::lower_bound(sl, sl + ln.n_slots, hi) - sl);
+                    if (bb >= ee) continue;
+                    const auto& h = pool.handle(plan.cseg_node[s]);
+                    const int64_t off = plan.cseg_offset[s], len = plan.cseg_len[s];
+                    for (int64_t k2 = 0; k2 < len; ++k2) {
+                        const int64_t tok = off + k2;
+                        const int32_t row = (int32_t)(h.pages[tok / P] * P + tok % P);
+                        if (g_open >= 0) {
+                            const uint32_t info = S.grp_info[g_open];
+                            const int cnt = (int)(info & 0xffu);
+                            if (cnt < 16 && S.grp_row[g_open] + cnt == row && (int)((info >> 8) & 0xfffu) == bb &&
+                                (int)(info >> 20) == ee) {
+                                S.grp_info[g_open] = grp_pack(cnt + 1, bb, ee);
+                                continue;
+                            }
+                        }
+                        if ((int32_t)S.grp_row.size() - tile_g0 == TG) close_tile(false);
+                        g_open = (int32_t)S.grp_row.size();
+                        S.grp_row.push_back(row);
+                        S.grp_info.push_back(grp_pack(1, bb, ee));
+                    }
+                }
+            }
+            close_tile(true);
+            ln.tile_end = (int32_t)S.tiles.size();
+            if (ln.tile_end > ln.tile_begin) lanes.push_back(ln);
+        }
+    }
+    S.n_lanes = (int32_t)lanes.size();
+
+    // ---- 3. CTA runs over the (head, lane, tile) sequence
+    const int n_tiles = (int)S.tiles.size();
+    std::vector<int64_t> tcost(n_tiles);
+    int64_t per_head = 0;
+    for (int i = 0; i < n_tiles; ++i) {
+        tcost[i] = 16LL * S.tiles[i].ng + opt.tile_cost;
+        per_head += tcost[i];
+        S.kv_rows_loaded += 16LL * S.tiles[i].ng * n_heads;
+    }
+    const int n_cta = std::max(1, opt.num_ctas);
+    const int64_t total = per_head * n_heads;
+    S.cta_begin.assign(1, 0);
+    std::vector<int32_t> tile_lane(n_tiles);
+    for (int li = 0; li < (int)lanes.size(); ++li)
+        for (int i = lanes[li].tile_begin; i < lanes[li].tile_end; ++i) tile_lane[i] = li;
+    {
+        int cta = 0;
+        int64_t acc = 0;
+        ItemDesc* open = nullptr;
+        for (int h = 0; h < n_heads; ++h) {
+            for (int i = 0; i < n_tiles; ++i) {
+                // boundary of CTA `cta` at cost (cta + 1) * total / n_cta (nearest tile edge)
+                while (cta < n_cta - 1 && 2 * (acc * n_cta) >= (2LL * (cta + 1) * total - tcost[i] * n_cta)) {
+                    S.cta_begin.push_back((int32_t)S.items.size());
+                    ++cta;
+                    open = nullptr;
+                }
+                const int li = tile_lane[i];
+                if (!open || open->head != h || open->lane != li) {
+                    ItemDesc it{};
+                    it.head = h;
+                    it.lane = li;
+                    it.tile_begin = i;
+                    it.tile_end = i;
+                    it.slot_begin = lanes[li].slot_begin;
+                    it.n_slots = lanes[li].n_slots;
+                    S.items.push_back(it);
+                    open = &S.items.back();
+                }
+                open->tile_end = i + 1;
+                acc += tcost[i];
+            }
+        }
+        while ((int)S.cta_begin.size() < n_cta + 1) S.cta_begin.push_back((int32_t)S.items.size());
     }
 
-    // span length: aim at ~2 waves of CTAs over all kv heads
-    int64_t span = opt.span_tokens;
-    if (span <= 0) {
-        const int64_t target_units = std::max<int64_t>(1, (2LL * opt.num_sms) / std::max(1, n_kv_heads_local));
-        span = std::max<int64_t>(plan.block_size, (work_tokens + target_units - 1) / target_units);
-    }
-
-    // --- greedy span merge
-    std::vector<OpenUnit> done, open;
-    std::vector<int32_t> tmp;
-    auto close_stale = [&](int chunk) {
-        for (std::size_t i = 0; i < open.size();) {
-            if (open[i].last_chunk < chunk - 1) {
-                done.push_back(std::move(open[i]));
-                open.erase(open.begin() + (long)i);
+    // ---- 4. outputs: touched slots, direct vs partial, merge lists
+    const int L = S.n_leaves;
+    std::vector<int32_t> cover((size_t)L * n_heads, 0);
+    std::vector<uint8_t> touched;
+    for (ItemDesc& it : S.items) {
+        touched.assign(it.n_slots, 0);
+        for (int i = it.tile_begin; i < it.tile_end; ++i) {
+            const TileDesc& td = S.tiles[i];
+            for (int g = 0; g < td.ng; ++g) {
+                const uint32_t info = S.grp_info[td.grp_begin + g];
+                for (int j = (int)((info >> 8) & 0xfffu); j < (int)(info >> 20); ++j) touched[j] = 1;
+            }
+        }
+        it.out_begin = (int32_t)S.slot_out.size();
+        for (int j = 0; j < it.n_slots; ++j) {
+            if (touched[j]) {
+                cover[(size_t)S.slot_leaf[it.slot_begin + j] * n_heads + it.head]++;
+                S.slot_out.push_back(0);
             } else {
-                ++i;
+                S.slot_out.push_back(kSlotUnused);
             }
         }
-    };
-    for (const Block& bl : blocks) {
-        close_stale(bl.chunk);
-        const int cap_rows = bl.mma ? opt.mma_max_rows : opt.fma_max_rows;
-        const int S_slots = std::max(1, cap_rows / G);
-        const int32_t* bq = plan.chunk_q.data() + bl.q0;
-        const int nb = bl.q1 - bl.q0;
-        int pick = -1;
-        for (std::size_t i = 0; i < open.size(); ++i) {
-            OpenUnit& u = open[i];
-            if (u.mma != bl.mma || u.last_chunk != bl.chunk - 1) continue;
-            if (u.tokens + bl.tokens > span) continue;
-            // MMA units keep their group metadata in SMEM: <= kMaxUnitGroups boxes
-            if (u.mma && u.grp_est + bl.grp_est > kMaxUnitGroups) continue;
-            sorted_union(u.slots, bq, nb, tmp);
-            if ((int)tmp.size() > S_slots) continue;
-            // prefer exact continuation of the same query block
-            if (pick < 0 || (int)tmp.size() == (int)u.slots.size()) pick = (int)i;
-        }
-        if (pick < 0) {
-            open.emplace_back();
-            open.back().mma = bl.mma;
-            pick = (int)open.size() - 1;
-        }
-        OpenUnit& u = open[pick];
-        sorted_union(u.slots, bq, nb, tmp);
-        u.slots = tmp;
-        for (int s = plan.chunk_seg_begin[bl.chunk]; s < plan.chunk_seg_begin[bl.chunk + 1]; ++s)
-            if (plan.cseg_hi[s] > bq[0] && plan.cseg_lo[s] <= bq[nb - 1]) {
-                // the segment's interval must intersect the block itself
-                const int32_t* lo_it = std::lower_bound(bq, bq + nb, plan.cseg_lo[s]);
-                if (lo_it == bq + nb || *lo_it >= plan.cseg_hi[s]) continue;
-                // attended only by this chunk's block: the unit may hold other
-                // slots (from neighbouring chunks) that belong to a sibling block here
-                u.pieces.push_back({plan.cseg_node[s], plan.cseg_offset[s], plan.cseg_len[s],
-                                    std::max(plan.cseg_lo[s], bq[0]), std::min(plan.cseg_hi[s], bq[nb - 1] + 1)});
-                u.tokens += plan.cseg_len[s];
-            }
-        u.grp_est += bl.grp_est;
-        u.last_chunk = bl.chunk;
     }
-    for (auto& u : open) done.push_back(std::move(u));
-
-    // --- leaf coverage counts -> direct vs partial
-    std::vector<int32_t> cover(S.n_leaves, 0);
-    for (const auto& u : done)
-        for (int32_t l : u.slots) cover[l]++;
-
-    std::vector<std::vector<int32_t>> leaf_parts(S.n_leaves);
-    auto emit = [&](const OpenUnit& u, std::vector<UnitDesc>& dst) {
-        UnitDesc d;
-        d.tok_begin = (int32_t)S.tok_row.size();
-        d.slot_begin = (int32_t)S.slot_leaf.size();
-        d.n_slots = (int32_t)u.slots.size();
-        for (int32_t l : u.slots) {
-            S.slot_leaf.push_back(l);
-            if (opt.final_direct && cover[l] == 1) {
-                S.slot_part.push_back(-1 - l);
-            } else {
-                leaf_parts[l].push_back(S.n_partials);
-                S.slot_part.push_back(S.n_partials++);
+    std::vector<int32_t> rec((size_t)L * n_heads, -1);  // leaf-head -> merge record
+    std::vector<std::vector<int32_t>> rec_parts;
+    for (const ItemDesc& it : S.items) {
+        for (int j = 0; j < it.n_slots; ++j) {
+            int32_t& code = S.slot_out[it.out_begin + j];
+            if (code == kSlotUnused) continue;
+            const int32_t leaf = S.slot_leaf[it.slot_begin + j];
+            const size_t key = (size_t)leaf * n_heads + it.head;
+            if (opt.final_direct && cover[key] == 1) {
+                code = -1 - leaf;
+                continue;
             }
-        }
-        for (const Piece& pc : u.pieces) {
-            const int b = (int)(std::lower_bound(u.slots.begin(), u.slots.end(), pc.lo) - u.slots.begin());
-            const int e = (int)(std::lower_bound(u.slots.begin(), u.slots.end(), pc.hi) - u.slots.begin());
-            const auto& h = pool.handle(pc.node);
-            for (int64_t k = 0; k < pc.len; ++k) {
-                const int64_t tok = pc.off + k;
-                S.tok_row.push_back((int32_t)(h.pages[tok / P] * P + tok % P));
-                S.tok_be.push_back((uint32_t)b | ((uint32_t)e << 16));
+            if (rec[key] < 0) {
+                rec[key] = (int32_t)rec_parts.size();
+                rec_parts.emplace_back();
+                S.merge_leaf.push_back(leaf);
+                S.merge_head.push_back(it.head);
             }
+            code = S.n_partials++;
+            S.part_merge.push_back(rec[key]);
+            rec_parts[rec[key]].push_back(code);
         }
-        d.n_tokens = (int32_t)(S.tok_row.size() - d.tok_begin);
-        S.kv_tokens_loaded += d.n_tokens;
-        d.grp_begin = (int32_t)S.grp_row.size();
-        d.n_grp = 0;
-        d.pad0 = d.pad1 = 0;
-        if (u.mma) {
-            for (int32_t k = d.tok_begin; k < d.tok_begin + d.n_tokens;) {
-                const int32_t row0 = S.tok_row[k];
-                const uint32_t be = S.tok_be[k];
-                int cnt = 1;
-                while (cnt < 16 && k + cnt < d.tok_begin + d.n_tokens && S.tok_row[k + cnt] == row0 + cnt &&
-                       S.tok_be[k + cnt] == be)
-                    ++cnt;
-                S.grp_row.push_back(row0);
-                S.grp_info.push_back(grp_pack(cnt, (int)(be & 0xffffu), (int)(be >> 16)));
-                k += cnt;
-            }
-            d.n_grp = (int32_t)S.grp_row.size() - d.grp_begin;
-            if (d.n_grp > kMaxUnitGroups) fail(TA_ERR_LOGIC, "schedule: MMA unit exceeds its group capacity");
-            S.kv_tokens_loaded += 16LL * d.n_grp - d.n_tokens;  // box over-read
-        }
-        dst.push_back(d);
-    };
-    for (const auto& u : done) emit(u, u.mma ? S.units_mma : S.units_fma);
-
-    S.merge_begin.push_back(0);
-    for (int32_t l = 0; l < S.n_leaves; ++l) {
-        if (opt.final_direct && cover[l] == 1) continue;
-        S.merge_leaf.push_back(l);
-        S.merge_parts.insert(S.merge_parts.end(), leaf_parts[l].begin(), leaf_parts[l].end());
+    }
+    for (ItemDesc& it : S.items)
+        for (int j = 0; j < it.n_slots; ++j)
+            if (S.slot_out[it.out_begin + j] >= 0) it.pad |= 1;   // holds partials: takes part in merges
+    S.merge_begin.assign(1, 0);
+    for (const auto& v : rec_parts) {
+        S.merge_parts.insert(S.merge_parts.end(), v.begin(), v.end());
         S.merge_begin.push_back((int32_t)S.merge_parts.size());
     }
+    for (int32_t l = 0; l < L; ++l)
+        for (int h = 0; h < n_heads; ++h)
+            if (cover[(size_t)l * n_heads + h] == 0) {
+                S.empty.push_back(l);
+                S.empty.push_back(h);
+            }
     for (int32_t l : t.leaves) S.masked_q_tokens += t.path_tokens(l);
 }
 

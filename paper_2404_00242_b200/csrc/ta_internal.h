@@ -122,58 +122,83 @@ void plan_flatten(const Tree& t, int block_size, Plan& out);   // partition.hpp:
 std::string plan_json(const Tree& t, const Plan& p);           // serde.hpp:41-61
 
 // ---------------------------------------------------------------------------
-// Device schedule (this framework's layout; see DESIGN.md §3).
-// A unit is one CTA's work for one kv head: a span of consecutive chunks and
-// a block of query slots (local slot j <-> leaf index unit_slot[slot_begin+j]).
-// Its tokens are listed in stream order; per token the row index inside a
-// (layer, head) slab (page * P + slot) and the local slot range [b, e) whose
-// queries attend it.
-struct UnitDesc {
-    int32_t tok_begin;   // into tok_row / tok_be
-    int32_t n_tokens;
-    int32_t slot_begin;  // into slot_leaf / slot_part
-    int32_t n_slots;
-    int32_t grp_begin;   // MMA units: into grp_row / grp_info
-    int32_t n_grp;
-    int32_t pad0, pad1;
+// Device schedule (this framework's layout; see DESIGN.md section 3).
+//
+//   stripe  a maximal run of consecutive flatten chunks whose query sets fit
+//           one row tile together (or, for chunks with more queries than a
+//           tile holds, runs of chunks with the identical query set)
+//   lane    one row block of a stripe: a fixed, sorted list of query slots
+//           (leaf indices, <= max_rows / G of them) and the stripe tokens any
+//           of those slots attend, cut into 16-row groups and tiles
+//   group   <= 16 tokens at consecutive pool rows with one attending slot
+//           range [b, e) (local slot indices of the lane): one TMA box row set
+//   tile    <= 8 groups (<= 128 tokens): one KV stage / one MMA N extent
+//   item    a run of tiles of one lane for one kv head, processed by one CTA
+//           with its (m, l, O) kept on chip; a CTA owns a contiguous run of
+//           the (head, lane, tile) sequence balanced by cost
+// Items whose leaf-head is covered by one item write the final output
+// directly; the rest write (O/l, log2 lse) partial records that the last
+// arriving CTA of that leaf-head merges (deterministic partial order).
+struct TileDesc {          // 16 bytes, read by the device
+    int32_t grp_begin;     // into grp_row / grp_info
+    uint8_t ng;            // groups in the tile (1..8)
+    uint8_t nbox;          // TMA boxes covering them
+    uint16_t ntok;         // real tokens
+    uint8_t box[8];        // (first group << 2) | log2(box rows / 16)
 };
+static_assert(sizeof(TileDesc) == 16, "TileDesc layout");
 
-// MMA units load KV as TMA boxes of 16 consecutive pool rows ("groups"):
-// a group is a run of <= 16 tokens with consecutive rows and one attending
-// slot range; rows of the box past `count` are masked.
+struct ItemDesc {          // 32 bytes, read by the device
+    int32_t head;          // local kv head
+    int32_t tile_begin, tile_end;
+    int32_t slot_begin;    // into slot_leaf (the lane's slots)
+    int32_t n_slots;
+    int32_t out_begin;     // into slot_out: one code per slot of the item
+    int32_t lane;
+    int32_t pad;
+};
+static_assert(sizeof(ItemDesc) == 32, "ItemDesc layout");
+
+constexpr int32_t kSlotUnused = INT32_MIN;   // slot_out: slot not attended in this item
+
 inline uint32_t grp_pack(int count, int b, int e) {
     return (uint32_t)count | ((uint32_t)b << 8) | ((uint32_t)e << 20);
 }
 
 struct Schedule {
-    std::vector<UnitDesc> units_fma, units_mma;
-    std::vector<int32_t> tok_row;     // page * P + slot
-    std::vector<uint32_t> tok_be;     // b | e << 16
+    std::vector<TileDesc> tiles;
     std::vector<int32_t> grp_row;     // first pool row of the group (page * P + slot)
     std::vector<uint32_t> grp_info;   // grp_pack(count, b, e)
-    std::vector<int32_t> slot_leaf;   // leaf index
-    std::vector<int32_t> slot_part;   // partial id, or -1 - leaf for direct final write
-    std::vector<int32_t> merge_leaf;  // leaves merged by the merge kernel
-    std::vector<int32_t> merge_begin; // [n_merge+1] into merge_parts
-    std::vector<int32_t> merge_parts; // partial ids in deterministic order
+    std::vector<ItemDesc> items;
+    std::vector<int32_t> cta_begin;   // [n_ctas + 1] into items
+    std::vector<int32_t> slot_leaf;   // lanes' slots: leaf index (leaves() order)
+    std::vector<int32_t> slot_out;    // per item slot: -1 - leaf (direct), partial id, or kSlotUnused
+    std::vector<int32_t> part_merge;  // partial id -> merge record
+    std::vector<int32_t> merge_leaf, merge_head;  // merge record -> leaf index, local kv head
+    std::vector<int32_t> merge_begin; // [n_merge + 1] into merge_parts
+    std::vector<int32_t> merge_parts; // partial ids in merge order (item order)
+    std::vector<int32_t> empty;       // [n][2] (leaf, local head) pairs with no path tokens
+    int32_t n_lanes = 0;
     int32_t n_partials = 0;
     int32_t n_leaves = 0;
-    int64_t kv_tokens_unique = 0;
-    int64_t kv_tokens_loaded = 0;
+    int64_t kv_tokens_unique = 0;     // per kv head
+    int64_t kv_rows_loaded = 0;       // box rows loaded, all local heads
     int64_t masked_q_tokens = 0;      // sum over leaves of path tokens (flops / (4 d h_q))
+    int64_t n_stripes = 0;
 };
 
 struct SchedOptions {
-    int fma_max_rows = 8;      // rows (= slots * G) above which a chunk goes to MMA
-    int mma_max_rows = 128;    // rows per MMA unit (one TMEM row tile)
-    bool use_mma = true;       // bf16 only
-    int span_tokens = 0;       // 0 = auto
-    bool final_direct = true;  // single-partial leaves written directly
-    int num_sms = 148;
-    int64_t trace_ptr = 0;     // debug: device buffer for the MMA kernel's clock64 trace
+    int max_rows = 128;        // rows (slots x G) per lane: 128 for the MMA kernel, 8/16 for FMA
+    int tile_groups = 8;       // groups per tile
+    int num_ctas = 148;        // persistent grid
+    int tile_cost = 24;        // fixed per-tile cost, in box rows
+    bool use_mma = true;       // bf16 d128 only
+    int fma_max_rows = 8;      // rows per lane of the FMA kernel (8 or 16)
+    bool final_direct = true;  // single-item leaf-heads written directly
+    int64_t trace_ptr = 0;     // debug: device buffer for the kernel's clock64 trace
 };
 
 void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int group_size,
-                    int n_kv_heads_local, bool bf16, const SchedOptions& opt, Schedule& out);
+                    int n_kv_heads_local, const SchedOptions& opt, Schedule& out);
 
 }  // namespace ta

@@ -9,64 +9,60 @@
 
 namespace ta {
 
-// One attention launch over a list of units for all local kv heads
-// (grid.y = kv head).  Rows of a unit are (slot, q-head-in-group) pairs,
-// row = slot * G + g; q head index (local) = kv_head * G + g.
+// One persistent launch per layer (grid = schedule CTAs, one per SM).  A CTA
+// walks its items (see ta_internal.h); rows of an item are (slot, q head in
+// the GQA group) pairs, row = slot * G + g, local q head = head * G + g.
 struct AttnArgs {
-    const void* k;            // layer base of the K pool, local kv head 0
+    // KV pools of this layer.  FMA path: element pointers + per-head stride.
+    const void* k;
     const void* v;
-    int64_t head_stride;      // elements between kv heads in the pool
-    const void* q;            // [L][hq_loc][D]
+    int64_t head_stride;      // elements between kv heads
+    // MMA path: TMA maps over the whole pools ([rows][D] bf16, rows =
+    // (layer * n_loc + head) * head_rows + page * P + slot)
+    const void* tmap_k;       // CUtensorMap[4] (16/32/64/128-row boxes), host memory
+    const void* tmap_v;
+    int64_t layer_row0;
+    int64_t head_rows;
+    // queries / outputs, leaves() order
+    const void* q;            // [L][hq_loc][D] kv dtype
     void* out;                // [L][hq_loc][D] out dtype
     float* lse;               // [L][hq_loc] natural log, or nullptr
-    float* part_o;            // [n_part][hq_loc][D]
-    float* part_lse;          // [n_part][hq_loc] (log2 domain)
-    const UnitDesc* units;
-    int n_units;
-    const int32_t* tok_row;
-    const uint32_t* tok_be;
+    float* part_o;            // [n_part][G][D] fp32, O / l
+    float* part_lse;          // [n_part][G] log2 domain
+    int* counters;            // [n_merge] arrivals, reset to 0 by the merging CTA
+    // schedule (device copies of Schedule)
+    const TileDesc* tiles;
+    const int32_t* grp_row;
+    const uint32_t* grp_info;
+    const ItemDesc* items;
+    const int32_t* cta_begin;
     const int32_t* slot_leaf;
-    const int32_t* slot_part;
+    const int32_t* slot_out;
+    const int32_t* part_merge;
+    const int32_t* merge_leaf;
+    const int32_t* merge_begin;
+    const int32_t* merge_parts;
+    const int32_t* empty;     // [n_empty][2] (leaf, head)
+    int n_empty;
+    int n_ctas;
     int G;
     int hq_loc;
-    int n_kv_loc;
     int D;
     float scale_log2;         // log2(e) / sqrt(D)
     int kv_bf16;
     int out_bf16;
-    // MMA path: TMA tensor maps over the whole K / V pools ([rows][D] bf16,
-    // rows = layer * n_loc * head_rows + head * head_rows + page * P + slot)
-    const void* tmap_k;       // CUtensorMap[4] (16/32/64/128-row boxes; host memory, copied into params)
-    const void* tmap_v;
-    int64_t layer_row0;
-    int64_t head_rows;
-    const int32_t* grp_row;
-    const uint32_t* grp_info;
-    long long* trace;         // optional per-tile clock64 trace of CTA (0,0)
+    long long* trace;         // optional clock64 trace (debug)
 };
 
-struct MergeArgs {
-    const float* part_o;
-    const float* part_lse;
-    const int32_t* merge_leaf;
-    const int32_t* merge_begin;
-    const int32_t* merge_parts;
-    int n_merge;
-    void* out;
-    float* lse;
-    int hq_loc;
-    int D;
-    int out_bf16;
-};
-
-// FMA path (sparse chunks / fp32): max_rows in {8, 16}.
-cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, cudaStream_t s);
-// tcgen05/TMEM path (dense bf16 chunks, D in {64,128}).
-cudaError_t launch_attn_mma(const AttnArgs& a, cudaStream_t s);
+// tcgen05/TMEM path (bf16, D = 128).
+cudaError_t launch_attn_mma(const AttnArgs& a, bool pdl, cudaStream_t s);
 bool mma_supported(int D, int kv_bf16);
 // encode the TMA descriptor (128 B, CUtensorMap) of a [rows][D] bf16 pool
 bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D, int box_rows);
-cudaError_t launch_merge(const MergeArgs& a, cudaStream_t s);
+// FMA path (fp32 or bf16, D in {16, 32, 64, 128}, rows per lane <= 8 or 16).
+cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, bool pdl, cudaStream_t s);
+// groups per tile the FMA kernel stages (2 stages of K and V fit in SMEM)
+int fma_tile_groups(int D, int esize);
 // dst rows[i] <- src row i, for n_loc kv heads: src [n][n_loc][D], dst pool
 cudaError_t launch_kv_scatter(const void* src_k, const void* src_v, void* dst_k, void* dst_v,
                               const int32_t* rows, int n, int n_loc, int64_t head_stride, int D,

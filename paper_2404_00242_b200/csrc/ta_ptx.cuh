@@ -1,0 +1,181 @@
+// ta_ptx.cuh -- sm_100a PTX helpers shared by the attention kernels
+// (mbarriers, TMA, tcgen05/TMEM, PDL) and the last-arriver partial merge.
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "ta_kernels.h"
+
+namespace ta {
+namespace dev {
+
+constexpr float kLn2 = 0.69314718055994530942f;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// ------------------------------------------------------------------ mbarrier
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+// ------------------------------------------------------------------ TMA
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ------------------------------------------------------------------ tcgen05
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// SMEM matrix descriptor, SWIZZLE_128B, sm_100 version bit.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// kind::f16 instruction descriptor: f32 accumulate, bf16 A/B, A/B major bits.
+__device__ __forceinline__ uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+#define TA_TMEM_LD16(addr, r)                                                                                  \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),         \
+                   "=r"(r[15])                                                                                  \
+                 : "r"(addr))
+#define TA_TMEM_ST16(addr, r)                                                                                  \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+                 ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), \
+                   "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])      \
+                 : "memory")
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// ------------------------------------------------------------------ misc
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Programmatic dependent launch: let the next launch on the stream start its
+// prologue now; wait for the previous launch's memory before touching shared
+// state (queries, outputs, partials, merge counters).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Store NV consecutive fp32 values (NV % 8 == 0) as the output dtype.
+template <int NV>
+__device__ __forceinline__ void store_row(void* out, size_t base, const float* v, float scale, int out_bf16) {
+    if (out_bf16) {
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + base);
+#pragma unroll
+        for (int i = 0; i < NV / 8; ++i)
+            dst[i] = make_uint4(pack_bf16(v[8 * i] * scale, v[8 * i + 1] * scale), pack_bf16(v[8 * i + 2] * scale, v[8 * i + 3] * scale),
+                                pack_bf16(v[8 * i + 4] * scale, v[8 * i + 5] * scale), pack_bf16(v[8 * i + 6] * scale, v[8 * i + 7] * scale));
+    } else {
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + base);
+#pragma unroll
+        for (int i = 0; i < NV / 4; ++i)
+            dst[i] = make_float4(v[4 * i] * scale, v[4 * i + 1] * scale, v[4 * i + 2] * scale, v[4 * i + 3] * scale);
+    }
+}
+
+// tree_reduce (attention.hpp:209-233) of NV columns [c0, c0+NV) of one
+// (leaf, q head) row from its partial records, in merge-list order; called
+// by the CTA whose arrival completed the record.  Partials were written by
+// other SMs: read through L2 (ld.global.cg).
+template <int NV>
+__device__ __forceinline__ void merge_row(const AttnArgs& a, int mi, int g, int hq, int leaf, int c0) {
+    const int pb = a.merge_begin[mi], pe = a.merge_begin[mi + 1];
+    float M = -INFINITY;
+    for (int p = pb; p < pe; ++p) M = fmaxf(M, __ldcg(a.part_lse + (size_t)a.merge_parts[p] * a.G + g));
+    float den = 0.f, acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+    for (int p = pb; p < pe; ++p) {
+        const int pid = a.merge_parts[p];
+        const float l2 = __ldcg(a.part_lse + (size_t)pid * a.G + g);
+        if (l2 == -INFINITY) continue;
+        const float w = ex2(l2 - M);
+        den += w;
+        const float4* src = reinterpret_cast<const float4*>(a.part_o + ((size_t)pid * a.G + g) * a.D + c0);
+#pragma unroll
+        for (int i = 0; i < NV / 4; ++i) {
+            const float4 o = __ldcg(src + i);
+            acc[4 * i] += w * o.x;
+            acc[4 * i + 1] += w * o.y;
+            acc[4 * i + 2] += w * o.z;
+            acc[4 * i + 3] += w * o.w;
+        }
+    }
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    store_row<NV>(a.out, ((size_t)leaf * a.hq_loc + hq) * a.D + c0, acc, inv, a.out_bf16);
+    if (c0 == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
+}
+
+// Leaf-heads whose path holds no tokens: out = 0, lse = -inf (they are
+// absent from the reference's AttentionOutput).  One warp, strided over CTAs.
+__device__ __forceinline__ void fill_empty(const AttnArgs& a, int lane) {
+    for (int e = blockIdx.x; e < a.n_empty; e += gridDim.x) {
+        const int leaf = a.empty[2 * e], head = a.empty[2 * e + 1];
+        const size_t base = ((size_t)leaf * a.hq_loc + (size_t)head * a.G) * a.D;
+        for (int i = lane; i < a.G * a.D; i += 32) {
+            if (a.out_bf16)
+                reinterpret_cast<__nv_bfloat16*>(a.out)[base + i] = __float2bfloat16_rn(0.f);
+            else
+                reinterpret_cast<float*>(a.out)[base + i] = 0.f;
+        }
+        if (a.lse)
+            for (int g = lane; g < a.G; g += 32) a.lse[(size_t)leaf * a.hq_loc + head * a.G + g] = -INFINITY;
+    }
+}
+
+}  // namespace dev
+}  // namespace ta

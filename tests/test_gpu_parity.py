@@ -121,15 +121,16 @@ def test_zero_token_nodes_and_empty_paths():
 
 
 def test_fma_row_limits():
-    """Same answers whatever the FMA row capacity (units re-split)."""
+    """Same answers whatever the FMA row capacity and CTA count (items re-split,
+    more partials and last-arriver merges)."""
     rng = core.Rng(5)
     t = core.random_tree(rng, max_leaves=40)
     c = make_content(t, 128, 4, 4, 1, bf16=False)
     ref = core.naive_attention(t, c, 128, 4)
     for rows in (4, 8, 16):
-        for span in (0, 128, 100000):
+        for ctas in (1, 7, 148, 600):
             out, _, _ = run_gpu(t.snapshot(), c, 128, 4, 4, "f32", 128,
-                                options={"fma_max_rows": rows, "span_tokens": span})
+                                options={"fma_max_rows": rows, "num_ctas": ctas})
             check_fp32(out, ref)
 
 
@@ -223,3 +224,40 @@ def test_multilayer_and_host_entry():
         oh = np.zeros((len(leaves), 8, 128), np.float32)
         ctx.attend_host(l, qh, oh)
         assert np.array_equal(oh.reshape(len(leaves), -1), out)
+
+
+# ------------------------------------------------------- schedule variations
+def test_mma_cta_counts_and_fma_bf16():
+    """The tcgen05 kernel with 1..600 CTAs (long items, many partials) and the
+    FMA kernel on the same bf16 inputs."""
+    rng = core.Rng(31)
+    t = core.random_tree(rng, max_leaves=60, max_node_tokens=300)
+    for opts in ({"num_ctas": 1}, {"num_ctas": 7}, {"num_ctas": 600}, {"tile_groups": 3},
+                 {"use_mma": 0, "fma_max_rows": 8}, {"use_mma": 0, "fma_max_rows": 16}):
+        _gqa_case(t, 128, 32, 8, 13, options=opts)
+
+
+def test_wide_mha_bf16():
+    """MHA bf16 with > 128 leaves sharing a prefix: wide stripes, 128-slot lanes."""
+    t = core.Tree(640)
+    t.branch(t.root, [1] * 150)
+    _gqa_case(t, 128, 2, 2, 17)
+
+
+def test_repeat_launches_deterministic():
+    """Back-to-back launches (PDL on) reuse the self-resetting merge counters:
+    every launch returns bit-identical outputs."""
+    import torch
+    t = core.Tree(3000)
+    kids = t.branch(t.root, [0] * 20)
+    for k in kids:
+        t.append_tokens(k, 150)
+    c = make_content(t, 128, 32, 8, 2, bf16=True)
+    out, _, ctx = run_gpu(t.snapshot(), c, 128, 32, 8, "bf16", 128, options={"num_ctas": 148})
+    leaves = ctx.leaves()
+    q = q_tensor(ctx, c, leaves)
+    outs = [ctx.attend(0, q) for _ in range(6)]
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, outs[0])
+    assert np.array_equal(outs[0].float().cpu().numpy().reshape(len(leaves), -1), out)

@@ -12,10 +12,12 @@ import pytest
 from oracle import core
 from paper_2404_00242_b200 import TreeAttention
 
+UNUSED = -(1 << 31)
 
-def _ctx(G=1, dtype="f32"):
-    # bf16 + d_head 128 routes dense chunks to MMA units
-    return TreeAttention(device=-1, n_q_heads=G, n_kv_heads=1, d_head=128 if dtype == "bf16" else 16,
+
+def _ctx(G=1, dtype="f32", n_kv=1):
+    # bf16 + d_head 128 selects the tcgen05 kernel's schedule (128-row lanes)
+    return TreeAttention(device=-1, n_q_heads=G * n_kv, n_kv_heads=n_kv, d_head=128 if dtype == "bf16" else 16,
                          kv_dtype=dtype)
 
 
@@ -29,10 +31,17 @@ def _row_map(ctx, snap):
     return m
 
 
-def _units(S):
-    for u in range(len(S["kind"])):
-        tb, nt, sb, ns = (int(x) for x in S["desc"][u])
-        yield u, tb, nt, sb, ns
+def _items(S):
+    for i, it in enumerate(S["items"]):
+        head, tb, te, sb, ns, ob, lane, flags = (int(x) for x in it)
+        yield i, head, tb, te, sb, ns, ob, flags
+
+
+def _groups(S, t):
+    g0 = int(S["tile_grp_begin"][t])
+    for g in range(g0, g0 + int(S["tile_ng"][t])):
+        info = int(S["grp_info"][g])
+        yield g, int(S["grp_row"][g]), info & 0xFF, (info >> 8) & 0xFFF, info >> 20
 
 
 def check_coverage(ctx, tree: core.Tree, bs):
@@ -40,50 +49,77 @@ def check_coverage(ctx, tree: core.Tree, bs):
     S = ctx.schedule(bs)
     rows = _row_map(ctx, snap)
     leaves = list(tree.leaves())
+    n_heads = ctx.n_local_kv_heads
+    max_rows = 128 if S["use_mma"] else 16
+    cb = S["cta_begin"]
+    assert cb[0] == 0 and cb[-1] == len(S["items"]) and np.all(np.diff(cb) >= 0)
     seen = {}
-    slot_units = {}
-    for u, tb, nt, sb, ns in _units(S):
+    codes = {}
+    tile_use = {}
+    for i, head, tb, te, sb, ns, ob, flags in _items(S):
         slots = [int(x) for x in S["slot_leaf"][sb:sb + ns]]
         assert slots == sorted(slots) and len(set(slots)) == len(slots)
+        assert 0 < ns and ns * ctx.group <= max_rows and tb < te
         used = set()
-        for k in range(tb, tb + nt):
-            node, tok = rows[int(S["tok_row"][k])]
-            b, e = int(S["tok_be"][k]) & 0xFFFF, int(S["tok_be"][k]) >> 16
-            assert 0 <= b < e <= ns
-            for j in range(b, e):
-                li = slots[j]
-                used.add(j)
-                key = (li, node, tok)
-                seen[key] = seen.get(key, 0) + 1
-                assert tree.path_tokens(leaves[li]) > 0
-        assert used == set(range(ns)), "every slot of a unit attends something"
+        for t in range(tb, te):
+            tile_use[(head, t)] = tile_use.get((head, t), 0) + 1
+            ng = int(S["tile_ng"][t])
+            assert 1 <= ng <= 8
+            # TMA boxes: power-of-two runs of full, row-contiguous groups covering 0..ng-1 once
+            cover = []
+            for bx in S["tile_boxes"][t][:int(S["tile_nbox"][t])]:
+                g, sz = int(bx) >> 2, int(bx) & 3
+                cover += list(range(g, g + (1 << sz)))
+                gs = list(_groups(S, t))
+                for k in range(1, 1 << sz):
+                    assert gs[g + k - 1][2] == 16 and gs[g + k][1] == gs[g][1] + 16 * k
+            assert cover == list(range(ng))
+            for g, row0, cnt, b, e in _groups(S, t):
+                assert 1 <= cnt <= 16 and 0 <= b < e <= ns
+                for k in range(cnt):
+                    node, tok = rows[row0 + k]
+                    for j in range(b, e):
+                        used.add(j)
+                        key = (head, slots[j], node, tok)
+                        seen[key] = seen.get(key, 0) + 1
+        assert bool(flags & 1) == any(int(c) >= 0 for c in S["slot_out"][ob:ob + ns])
         for j in range(ns):
-            slot_units.setdefault(slots[j], []).append(int(S["slot_part"][sb + j]))
-    # exactly once, exactly the path
+            code = int(S["slot_out"][ob + j])
+            if j in used:
+                assert code != UNUSED
+                codes.setdefault((slots[j], head), []).append(code)
+            else:
+                assert code == UNUSED
+    n_tiles = len(S["tile_ng"])
+    assert all(tile_use.get((h, t)) == 1 for h in range(n_heads) for t in range(n_tiles))
+    # exactly once, exactly the path, for every head
     for li, leaf in enumerate(leaves):
         path = []
         cur = int(leaf)
         while cur != -1:
             path += [(cur, t) for t in range(tree.token_count(cur))]
             cur = tree.parent(cur)
-        got = {(n, t): c for (l, n, t), c in seen.items() if l == li}
-        assert set(got) == set(path), li
-        assert all(c == 1 for c in got.values()), li
-    # outputs: direct writes once, or partials merged
-    merged = {int(l): [int(p) for p in S["merge_parts"][S["merge_begin"][i]:S["merge_begin"][i + 1]]]
-              for i, l in enumerate(S["merge_leaf"])}
-    for li in range(len(leaves)):
-        parts = slot_units.get(li, [])
-        if len(parts) == 1 and parts[0] < 0:
-            assert parts[0] == -1 - li and li not in merged
+        for h in range(n_heads):
+            got = {(n, t): c for (hh, l, n, t), c in seen.items() if l == li and hh == h}
+            assert set(got) == set(path), (li, h)
+            assert all(c == 1 for c in got.values()), (li, h)
+    # outputs: one direct write, or partials merged in one record
+    recs = {(int(S["merge_leaf"][m]), int(S["merge_head"][m])): m for m in range(len(S["merge_leaf"]))}
+    for (li, h), cs in codes.items():
+        if len(cs) == 1:
+            assert cs[0] == -1 - li and (li, h) not in recs
         else:
-            assert all(p >= 0 for p in parts)
-            assert sorted(merged[li]) == sorted(parts)
+            m = recs[(li, h)]
+            parts = [int(p) for p in S["merge_parts"][S["merge_begin"][m]:S["merge_begin"][m + 1]]]
+            assert sorted(parts) == sorted(cs) and all(int(S["part_merge"][p]) == m for p in parts)
+    empty = {(int(l), int(h)) for l, h in S["empty"]}
+    assert empty == {(li, h) for li in range(len(leaves)) for h in range(n_heads) if (li, h) not in codes}
+    assert all(tree.path_tokens(leaves[li]) == 0 for li, h in empty)
     return S
 
 
 def interpret(ctx, tree, content, d, h_q, h_kv, bs):
-    """fp64 execution of the schedule (unit online softmax + merge)."""
+    """fp64 execution of the schedule (item online softmax + merge), one kv head."""
     S = ctx.schedule(bs)
     rows = _row_map(ctx, tree.snapshot())
     leaves = list(tree.leaves())
@@ -91,15 +127,18 @@ def interpret(ctx, tree, content, d, h_q, h_kv, bs):
     L = len(leaves)
     out = np.zeros((L, h_q, d))
     parts = {}
-    for u, tb, nt, sb, ns in _units(S):
+    for i, head, tb, te, sb, ns, ob, flags in _items(S):
         slots = [int(x) for x in S["slot_leaf"][sb:sb + ns]]
         for j, li in enumerate(slots):
+            code = int(S["slot_out"][ob + j])
+            if code == UNUSED:
+                continue
             q = content.queries[int(leaves[li])].astype(np.float64).reshape(h_q, d)
             toks = []
-            for k in range(tb, tb + nt):
-                b, e = int(S["tok_be"][k]) & 0xFFFF, int(S["tok_be"][k]) >> 16
-                if b <= j < e:
-                    toks.append(rows[int(S["tok_row"][k])])
+            for t in range(tb, te):
+                for g, row0, cnt, b, e in _groups(S, t):
+                    if b <= j < e:
+                        toks += [rows[row0 + k] for k in range(cnt)]
             K = np.stack([content.keys[n][t] for n, t in toks]).astype(np.float64).reshape(-1, h_kv, d)
             V = np.stack([content.values[n][t] for n, t in toks]).astype(np.float64).reshape(-1, h_kv, d)
             hk = np.arange(h_q) // G
@@ -108,27 +147,25 @@ def interpret(ctx, tree, content, d, h_q, h_kv, bs):
             w = np.exp(s - m)
             o = np.einsum("ht,thd->hd", w / w.sum(1, keepdims=True), V[:, hk])
             lse = (m + np.log(w.sum(1, keepdims=True))).ravel()
-            pid = int(S["slot_part"][sb + j])
-            if pid < 0:
-                out[-1 - pid] = o
+            if code < 0:
+                out[-1 - code] = o
             else:
-                parts[pid] = (o, lse)
-    for i, li in enumerate(S["merge_leaf"]):
-        ps = [parts[int(p)] for p in S["merge_parts"][S["merge_begin"][i]:S["merge_begin"][i + 1]]]
-        if not ps:
-            continue
+                parts[code] = (o, lse)
+    for m_i, li in enumerate(S["merge_leaf"]):
+        ps = [parts[int(p)] for p in S["merge_parts"][S["merge_begin"][m_i]:S["merge_begin"][m_i + 1]]]
         M = np.max([p[1] for p in ps], axis=0)
         w = [np.exp(p[1] - M) for p in ps]
         out[int(li)] = sum(wi[:, None] * p[0] for wi, p in zip(w, ps)) / sum(w)[:, None]
     return out.reshape(L, -1)
 
 
-@pytest.mark.parametrize("rows,span", [(8, 0), (4, 128), (16, 100000), (1, 0), (8, 1)])
-def test_coverage_random_trees(rows, span):
+@pytest.mark.parametrize("rows,ctas", [(8, 148), (4, 7), (16, 1), (1, 148), (8, 1000)])
+def test_coverage_random_trees(rows, ctas):
     ctx = _ctx(G=1)
+    ctx.set_option("use_mma", 0)
     ctx.set_option("fma_max_rows", rows)
-    ctx.set_option("span_tokens", span)
-    rng = core.Rng(900 + rows + span)
+    ctx.set_option("num_ctas", ctas)
+    rng = core.Rng(900 + rows + ctas)
     for trial in range(25):
         t = core.random_tree(rng, max_leaves=70 if trial % 2 else 12, max_node_tokens=40 if trial % 3 else 300,
                              mutation_steps=40)
@@ -140,14 +177,31 @@ def test_coverage_random_trees(rows, span):
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_coverage_gqa_groups(dtype):
     for G in (2, 4, 8):
-        ctx = _ctx(G=G, dtype=dtype)
+        ctx = _ctx(G=G, dtype=dtype, n_kv=3)
+        ctx.set_option("num_ctas", 37)
         rng = core.Rng(G)
         for trial in range(10):
             t = core.random_tree(rng, max_leaves=40)
             ctx.restore(*t.snapshot())
             S = check_coverage(ctx, t, 128)
-            if dtype == "bf16" and len(t.leaves()) * G > 8:
-                assert (S["kind"] == 1).any(), "dense chunks go to the MMA path"
+            assert S["use_mma"] == (dtype == "bf16")
+
+
+def test_coverage_wide_stripes_mma():
+    """>128 rows: wide stripes split into balanced slot blocks (MMA lanes)."""
+    ctx = _ctx(G=4, dtype="bf16", n_kv=2)
+    rng = core.Rng(5)
+    for trial in range(6):
+        t = core.random_tree(rng, max_leaves=120, max_node_tokens=200)
+        ctx.restore(*t.snapshot())
+        S = check_coverage(ctx, t, 128)
+    t = core.Tree(4000)
+    kids = t.branch(t.root, [0] * 50)
+    for k in kids:
+        t.append_tokens(k, 400)
+    ctx.restore(*t.snapshot())
+    S = check_coverage(ctx, t, 128)
+    assert S["n_lanes"] >= 2
 
 
 def test_coverage_zero_token_and_holders():
@@ -165,6 +219,7 @@ def test_interpreter_matches_oracle():
         G = (1, 2, 4)[trial % 3]
         ctx = _ctx(G=G)
         ctx.set_option("fma_max_rows", (4, 8, 16)[trial % 3])
+        ctx.set_option("num_ctas", (3, 50, 148)[trial % 3])
         t = core.random_tree(rng, max_leaves=30, max_tokens=2000, max_node_tokens=150)
         ctx.restore(*t.snapshot())
         c = core.Content.synth(t, 16, trial, qdim=16 * G)
