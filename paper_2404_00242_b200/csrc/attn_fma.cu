@@ -14,7 +14,7 @@
 //   P    exp2 online softmax; P goes through a per-warp SMEM buffer and is
 //        read back as broadcasts for O += P V (lane owns D/32 dims)
 // The warps' states are merged once per item, then written as the final
-// output or a partial with the same last-arriver merge as the MMA kernel.
+// output or as a partial record for merge.cu.
 //
 // Reference semantics: group_attention (attention.hpp:117-204) and
 // tree_reduce (attention.hpp:209-233).
@@ -327,54 +327,6 @@ __global__ void __launch_bounds__(256, 1) attn_fma_kernel(const AttnArgs a) {
             } else {
                 a.part_o[((size_t)code * G + gq) * D + d] = O;
                 if (d == 0) a.part_lse[(size_t)code * G + gq] = lse2;
-            }
-        }
-        if (I.pad & 1) {
-            // last-arriver merge: one thread per slot takes the ticket
-            __threadfence();
-            __syncthreads();
-            int* flag = reinterpret_cast<int*>(l_s);   // l_s consumed above
-            if (tid < I.n_slots) {
-                const int code = a.slot_out[I.out_begin + tid];
-                int f = 0;
-                if (code >= 0) {
-                    const int mi = a.part_merge[code];
-                    const int need = a.merge_begin[mi + 1] - a.merge_begin[mi];
-                    if (atomicAdd(a.counters + mi, 1) == need - 1) {
-                        a.counters[mi] = 0;   // self-reset for the next launch
-                        f = 1;
-                    }
-                }
-                flag[tid] = f;
-            }
-            __syncthreads();
-            for (int idx = tid; idx < nrows * D; idx += 256) {
-                const int r = idx / D, d = idx % D;
-                const int j = r / G, gq = r % G;
-                if (!flag[j]) continue;
-                __threadfence();
-                const int mi = a.part_merge[a.slot_out[I.out_begin + j]];
-                const int pb = a.merge_begin[mi], pe = a.merge_begin[mi + 1];
-                float M = -INFINITY;
-                for (int p = pb; p < pe; ++p) M = fmaxf(M, __ldcg(a.part_lse + (size_t)a.merge_parts[p] * G + gq));
-                float den = 0.f, O = 0.f;
-                for (int p = pb; p < pe; ++p) {
-                    const int pid = a.merge_parts[p];
-                    const float l2 = __ldcg(a.part_lse + (size_t)pid * G + gq);
-                    if (l2 == -INFINITY) continue;
-                    const float w = ex2(l2 - M);
-                    den += w;
-                    O += w * __ldcg(a.part_o + ((size_t)pid * G + gq) * D + d);
-                }
-                const int leaf = a.merge_leaf[mi], hq = I.head * G + gq;
-                const size_t o = ((size_t)leaf * a.hq_loc + hq) * D + d;
-                const float val = den > 0.f ? O / den : 0.f;
-                if (a.out_bf16)
-                    reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(val);
-                else
-                    reinterpret_cast<float*>(a.out)[o] = val;
-                if (d == 0 && a.lse)
-                    a.lse[(size_t)leaf * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
             }
         }
         __syncthreads();   // acc_s / m_s / l_s reuse

@@ -52,28 +52,28 @@ struct ta_ctx {
     size_t meta_host_cap = 0;
     cudaEvent_t meta_done = nullptr;
     const TileDesc* d_tiles = nullptr;
+    const TileMeta* d_tile_meta = nullptr;
     const int32_t* d_grp_row = nullptr;
     const uint32_t* d_grp_info = nullptr;
     const ItemDesc* d_items = nullptr;
     const int32_t* d_cta_begin = nullptr;
     const int32_t* d_slot_leaf = nullptr;
     const int32_t* d_slot_out = nullptr;
-    const int32_t* d_part_merge = nullptr;
+    const int32_t* d_merge_head = nullptr;
     const int32_t* d_merge_leaf = nullptr;
     const int32_t* d_merge_begin = nullptr;
     const int32_t* d_merge_parts = nullptr;
     const int32_t* d_empty = nullptr;
     bool pdl = true;
+    int64_t trace = 0;  // debug: device buffer for the MMA kernel's pipeline trace
     int num_sms = 148;
 
     // host copy of the schedule for ta_schedule_get
     Schedule dbg_sched;
 
-    // partial scratch + merge counters (self-resetting, zeroed on allocation)
+    // partial scratch
     float* part = nullptr;
     size_t part_cap = 0;  // floats
-    int* counters = nullptr;
-    size_t counters_cap = 0;  // bytes
 
     // staging for kv writes and host-buffer attend
     void* stage_dev = nullptr;
@@ -91,7 +91,6 @@ struct ta_ctx {
             cudaFree(meta_dev);
             cudaFreeHost(meta_host);
             cudaFree(part);
-            cudaFree(counters);
             cudaFree(stage_dev);
             cudaFreeHost(stage_host);
             cudaFree(io_dev);
@@ -253,6 +252,8 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->opt.final_direct = v != 0;
         } else if (k == "pdl") {
             c->pdl = v != 0;
+        } else if (k == "trace_ptr") {
+            c->trace = v;
         } else {
             fail(TA_ERR_INVALID_ARGUMENT, "unknown option " + k);
         }
@@ -459,15 +460,16 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             size_t bytes;
             size_t off;
         };
-        Part parts[12] = {
+        Part parts[13] = {
             {S.tiles.data(), S.tiles.size() * sizeof(TileDesc), 0},
+            {S.tile_meta.data(), S.tile_meta.size() * sizeof(TileMeta), 0},
             {S.grp_row.data(), S.grp_row.size() * 4, 0},
             {S.grp_info.data(), S.grp_info.size() * 4, 0},
             {S.items.data(), S.items.size() * sizeof(ItemDesc), 0},
             {S.cta_begin.data(), S.cta_begin.size() * 4, 0},
             {S.slot_leaf.data(), S.slot_leaf.size() * 4, 0},
             {S.slot_out.data(), S.slot_out.size() * 4, 0},
-            {S.part_merge.data(), S.part_merge.size() * 4, 0},
+            {S.merge_head.data(), S.merge_head.size() * 4, 0},
             {S.merge_leaf.data(), S.merge_leaf.size() * 4, 0},
             {S.merge_begin.data(), S.merge_begin.size() * 4, 0},
             {S.merge_parts.data(), S.merge_parts.size() * 4, 0},
@@ -490,17 +492,18 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         cuda_check(cudaEventRecord(c->meta_done, s), "cudaEventRecord");
         char* d = (char*)c->meta_dev;
         c->d_tiles = (const TileDesc*)(d + parts[0].off);
-        c->d_grp_row = (const int32_t*)(d + parts[1].off);
-        c->d_grp_info = (const uint32_t*)(d + parts[2].off);
-        c->d_items = (const ItemDesc*)(d + parts[3].off);
-        c->d_cta_begin = (const int32_t*)(d + parts[4].off);
-        c->d_slot_leaf = (const int32_t*)(d + parts[5].off);
-        c->d_slot_out = (const int32_t*)(d + parts[6].off);
-        c->d_part_merge = (const int32_t*)(d + parts[7].off);
-        c->d_merge_leaf = (const int32_t*)(d + parts[8].off);
-        c->d_merge_begin = (const int32_t*)(d + parts[9].off);
-        c->d_merge_parts = (const int32_t*)(d + parts[10].off);
-        c->d_empty = (const int32_t*)(d + parts[11].off);
+        c->d_tile_meta = (const TileMeta*)(d + parts[1].off);
+        c->d_grp_row = (const int32_t*)(d + parts[2].off);
+        c->d_grp_info = (const uint32_t*)(d + parts[3].off);
+        c->d_items = (const ItemDesc*)(d + parts[4].off);
+        c->d_cta_begin = (const int32_t*)(d + parts[5].off);
+        c->d_slot_leaf = (const int32_t*)(d + parts[6].off);
+        c->d_slot_out = (const int32_t*)(d + parts[7].off);
+        c->d_merge_head = (const int32_t*)(d + parts[8].off);
+        c->d_merge_leaf = (const int32_t*)(d + parts[9].off);
+        c->d_merge_begin = (const int32_t*)(d + parts[10].off);
+        c->d_merge_parts = (const int32_t*)(d + parts[11].off);
+        c->d_empty = (const int32_t*)(d + parts[12].off);
         // partial scratch: o [n_part][G][D] + lse [n_part][G]
         const size_t pf = (size_t)std::max(1, S.n_partials) * c->G * (c->shape.d_head + 1);
         if (pf > c->part_cap) {
@@ -509,15 +512,6 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             grow_dev(&p, &cap, pf * sizeof(float));
             c->part = (float*)p;
             c->part_cap = cap / sizeof(float);
-        }
-        const size_t cb = std::max<size_t>(1, S.merge_leaf.size()) * sizeof(int);
-        if (cb > c->counters_cap) {
-            // stream-ordered: earlier launches may still use the old array
-            cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-            void* p = c->counters;
-            grow_dev(&p, &c->counters_cap, cb);
-            c->counters = (int*)p;
-            cuda_check(cudaMemset(c->counters, 0, c->counters_cap), "cudaMemset(counters)");
         }
         c->prepared = true;
         c->prepared_version = c->tree.version;
@@ -544,16 +538,16 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.lse = lse;
     a.part_o = c->part;
     a.part_lse = c->part + (size_t)std::max(1, S.n_partials) * c->G * D;
-    a.counters = c->counters;
     a.tiles = c->d_tiles;
+    a.tile_meta = c->d_tile_meta;
     a.grp_row = c->d_grp_row;
     a.grp_info = c->d_grp_info;
     a.items = c->d_items;
     a.cta_begin = c->d_cta_begin;
     a.slot_leaf = c->d_slot_leaf;
     a.slot_out = c->d_slot_out;
-    a.part_merge = c->d_part_merge;
     a.merge_leaf = c->d_merge_leaf;
+    a.merge_head = c->d_merge_head;
     a.merge_begin = c->d_merge_begin;
     a.merge_parts = c->d_merge_parts;
     a.empty = c->d_empty;
@@ -565,11 +559,13 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     a.kv_bf16 = c->shape.kv_dtype == TA_BF16;
     a.out_bf16 = c->shape.out_dtype == TA_BF16;
+    a.trace = reinterpret_cast<long long*>(c->trace);
     const SchedOptions o = effective_opts(c);
     if (o.use_mma)
         cuda_check(launch_attn_mma(a, c->pdl, s), "attn_mma");
     else
         cuda_check(launch_attn_fma(a, o.fma_max_rows, c->pdl, s), "attn_fma");
+    cuda_check(launch_merge(a, (int)S.merge_leaf.size(), c->pdl, s), "merge");
 }
 
 ta_status ta_attend(ta_ctx* c, int layer, const void* q, void* out, float* lse, void* stream) {
@@ -614,9 +610,10 @@ ta_status ta_io_stats_get(ta_ctx* c, ta_io_stats* o) {
         o->q_bytes = L * c->hq_loc * D * c->esize;
         o->out_bytes = L * c->hq_loc * D * c->out_esize;
         o->partial_bytes = (int64_t)S.n_partials * c->G * (D + 1) * 4 * 2;
-        o->meta_bytes = (int64_t)(S.tiles.size() * sizeof(TileDesc) + S.items.size() * sizeof(ItemDesc)) +
+        o->meta_bytes = (int64_t)(S.tiles.size() * (sizeof(TileDesc) + sizeof(TileMeta)) +
+                                  S.items.size() * sizeof(ItemDesc)) +
                         (int64_t)(S.grp_row.size() + S.grp_info.size() + S.cta_begin.size() + S.slot_leaf.size() +
-                                  S.slot_out.size() + S.part_merge.size() + S.merge_leaf.size() +
+                                  S.slot_out.size() + S.merge_head.size() + S.merge_leaf.size() +
                                   S.merge_begin.size() + S.merge_parts.size() + S.empty.size()) * 4;
         o->flops = S.masked_q_tokens * c->hq_loc * 4 * D;
     });
@@ -658,7 +655,7 @@ ta_status ta_schedule_get(ta_ctx* c, int bs, ta_schedule_view* o) {
 
 int ta_launches_per_attend(ta_ctx* c) {
     if (!c || !c->prepared) return 0;
-    return 1;
+    return 1 + (c->sched.merge_leaf.empty() ? 0 : 1);
 }
 
 }  // extern "C"

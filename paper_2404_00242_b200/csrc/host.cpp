@@ -2,6 +2,7 @@
 // device schedule builder.  Reference citations are relative to
 // /root/reference/proj/include/treeattn.
 #include <algorithm>
+#include <cstring>
 #include <atomic>
 #include <cstdio>
 #include <numeric>
@@ -565,6 +566,15 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
         }
     }
     S.n_lanes = (int32_t)lanes.size();
+    S.tile_meta.resize(S.tiles.size());
+    for (std::size_t i = 0; i < S.tiles.size(); ++i) {
+        TileMeta& tm = S.tile_meta[i];
+        std::memset(&tm, 0, sizeof tm);
+        for (int g = 0; g < S.tiles[i].ng; ++g) {
+            tm.info[g] = S.grp_info[S.tiles[i].grp_begin + g];
+            tm.row[g] = S.grp_row[S.tiles[i].grp_begin + g];
+        }
+    }
 
     // ---- 3. CTA runs over the (head, lane, tile) sequence
     const int n_tiles = (int)S.tiles.size();

@@ -148,6 +148,14 @@ struct TileDesc {          // 16 bytes, read by the device
 };
 static_assert(sizeof(TileDesc) == 16, "TileDesc layout");
 
+// The tile's groups packed for single-load access by the device (no load
+// depends on another): slot ranges + counts, and first pool rows.
+struct TileMeta {          // 64 bytes
+    uint32_t info[8];      // grp_pack(count, b, e); 0 past ng
+    int32_t row[8];        // first pool row of each group
+};
+static_assert(sizeof(TileMeta) == 64, "TileMeta layout");
+
 struct ItemDesc {          // 32 bytes, read by the device
     int32_t head;          // local kv head
     int32_t tile_begin, tile_end;
@@ -167,6 +175,7 @@ inline uint32_t grp_pack(int count, int b, int e) {
 
 struct Schedule {
     std::vector<TileDesc> tiles;
+    std::vector<TileMeta> tile_meta;  // per tile, packed copy of its groups
     std::vector<int32_t> grp_row;     // first pool row of the group (page * P + slot)
     std::vector<uint32_t> grp_info;   // grp_pack(count, b, e)
     std::vector<ItemDesc> items;

@@ -29,17 +29,17 @@ struct AttnArgs {
     float* lse;               // [L][hq_loc] natural log, or nullptr
     float* part_o;            // [n_part][G][D] fp32, O / l
     float* part_lse;          // [n_part][G] log2 domain
-    int* counters;            // [n_merge] arrivals, reset to 0 by the merging CTA
     // schedule (device copies of Schedule)
     const TileDesc* tiles;
+    const TileMeta* tile_meta;
     const int32_t* grp_row;
     const uint32_t* grp_info;
     const ItemDesc* items;
     const int32_t* cta_begin;
     const int32_t* slot_leaf;
     const int32_t* slot_out;
-    const int32_t* part_merge;
     const int32_t* merge_leaf;
+    const int32_t* merge_head;
     const int32_t* merge_begin;
     const int32_t* merge_parts;
     const int32_t* empty;     // [n_empty][2] (leaf, head)
@@ -63,6 +63,8 @@ bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D, int b
 cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, bool pdl, cudaStream_t s);
 // groups per tile the FMA kernel stages (2 stages of K and V fit in SMEM)
 int fma_tile_groups(int D, int esize);
+// split-K merge of the partial records (after the attention launch)
+cudaError_t launch_merge(const AttnArgs& a, int n_merge, bool pdl, cudaStream_t s);
 // dst rows[i] <- src row i, for n_loc kv heads: src [n][n_loc][D], dst pool
 cudaError_t launch_kv_scatter(const void* src_k, const void* src_v, void* dst_k, void* dst_v,
                               const int32_t* rows, int n, int n_loc, int64_t head_stride, int D,

@@ -1,5 +1,5 @@
-// ta_ptx.cuh -- sm_100a PTX helpers shared by the attention kernels
-// (mbarriers, TMA, tcgen05/TMEM, PDL) and the last-arriver partial merge.
+// ta_ptx.cuh -- sm_100a PTX helpers shared by the kernels (mbarriers, TMA,
+// tcgen05/TMEM, PDL) and the empty-leaf fill.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -71,6 +71,13 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b
         " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// A operand from TMEM (K-major, bf16 pairs packed per 32-bit column, row = lane)
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -85,6 +92,10 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
                  ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), \
                    "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])      \
+                 : "memory")
+#define TA_TMEM_ST8(addr, r)                                                                                   \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(r[0]), \
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])                    \
                  : "memory")
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -106,7 +117,7 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 
 // Programmatic dependent launch: let the next launch on the stream start its
 // prologue now; wait for the previous launch's memory before touching shared
-// state (queries, outputs, partials, merge counters).
+// state (queries, outputs, partials).
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -125,39 +136,6 @@ __device__ __forceinline__ void store_row(void* out, size_t base, const float* v
         for (int i = 0; i < NV / 4; ++i)
             dst[i] = make_float4(v[4 * i] * scale, v[4 * i + 1] * scale, v[4 * i + 2] * scale, v[4 * i + 3] * scale);
     }
-}
-
-// tree_reduce (attention.hpp:209-233) of NV columns [c0, c0+NV) of one
-// (leaf, q head) row from its partial records, in merge-list order; called
-// by the CTA whose arrival completed the record.  Partials were written by
-// other SMs: read through L2 (ld.global.cg).
-template <int NV>
-__device__ __forceinline__ void merge_row(const AttnArgs& a, int mi, int g, int hq, int leaf, int c0) {
-    const int pb = a.merge_begin[mi], pe = a.merge_begin[mi + 1];
-    float M = -INFINITY;
-    for (int p = pb; p < pe; ++p) M = fmaxf(M, __ldcg(a.part_lse + (size_t)a.merge_parts[p] * a.G + g));
-    float den = 0.f, acc[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.f;
-    for (int p = pb; p < pe; ++p) {
-        const int pid = a.merge_parts[p];
-        const float l2 = __ldcg(a.part_lse + (size_t)pid * a.G + g);
-        if (l2 == -INFINITY) continue;
-        const float w = ex2(l2 - M);
-        den += w;
-        const float4* src = reinterpret_cast<const float4*>(a.part_o + ((size_t)pid * a.G + g) * a.D + c0);
-#pragma unroll
-        for (int i = 0; i < NV / 4; ++i) {
-            const float4 o = __ldcg(src + i);
-            acc[4 * i] += w * o.x;
-            acc[4 * i + 1] += w * o.y;
-            acc[4 * i + 2] += w * o.z;
-            acc[4 * i + 3] += w * o.w;
-        }
-    }
-    const float inv = den > 0.f ? 1.f / den : 0.f;
-    store_row<NV>(a.out, ((size_t)leaf * a.hq_loc + hq) * a.D + c0, acc, inv, a.out_bf16);
-    if (c0 == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
 }
 
 // Leaf-heads whose path holds no tokens: out = 0, lse = -inf (they are

@@ -7,7 +7,7 @@ python -m pytest tests -m gpu --collect-only -q -p no:cacheprovider 2>/dev/null 
 : > gpurun_out/isolate.log
 first=""
 while read id; do
-  if timeout 300 python -m pytest "$id" -q -x -p no:cacheprovider > gpurun_out/one.log 2>&1; then
+  if timeout 120 python -m pytest "$id" -q -x -p no:cacheprovider > gpurun_out/one.log 2>&1; then
     echo "PASS $id" >> gpurun_out/isolate.log
   else
     echo "FAIL $id" >> gpurun_out/isolate.log
@@ -20,3 +20,7 @@ if [ -n "$first" ]; then
   grep -E "Invalid|misaligned|at 0x|by thread|Address" gpurun_out/sanitizer.log | head -40
 fi
 cat gpurun_out/isolate.log
+if [ -n "$BENCH_ANYWAY" ]; then
+  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/bench.log 2>&1
+  tail -c 1500 gpurun_out/bench.log
+fi

@@ -1,51 +1,86 @@
-"""Per-tile pipeline trace of the MMA kernel's CTA (0,0) on the few-shot config."""
-import sys, os
+"""Pipeline trace of the persistent tcgen05 kernel on a bench config (debug).
+
+    python scripts/trace_mma.py [config] [option=value ...]
+
+Prints per-CTA durations (globaltimer) and per-tile pipeline events (clock64)
+of a few CTAs (see the TRACE comment in csrc/attn_mma.cu)."""
+import os
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import numpy as np
+import torch
+
 import bench
 from paper_2404_00242_b200 import TreeAttention
-cfg = dict(bench.CONFIGS["few_shot"]); cfg["n_layers"] = 2
+
+name = sys.argv[1] if len(sys.argv) > 1 and "=" not in sys.argv[1] else "few_shot"
+opts = [a for a in sys.argv[1:] if "=" in a]
+cfg = dict(bench.CONFIGS[name])
+cfg["n_layers"] = 2
 snap = bench.build_snapshot(cfg)
 root, ids, par, cnt = snap
-ctx = TreeAttention(n_layers=2, n_q_heads=32, n_kv_heads=8, d_head=128, kv_dtype="bf16", out_dtype="bf16",
-                    max_pages=int(sum((int(c)+15)//16 for c in cnt))+16)
-for kv in sys.argv[1:]:
-    k, v = kv.split("="); ctx.set_option(k, int(v))
+hkv, hq, d = cfg["h_kv"], cfg["h_q"], cfg["d"]
+ctx = TreeAttention(n_layers=2, n_q_heads=hq, n_kv_heads=hkv, d_head=d, kv_dtype="bf16", out_dtype="bf16",
+                    max_pages=int(sum((int(c) + 15) // 16 for c in cnt)) + 16)
+for kv in opts:
+    k, v = kv.split("=")
+    ctx.set_option(k, int(v))
 ctx.restore(*snap)
 for layer in range(2):
     for node, c in zip(ids, cnt):
         c = int(c)
-        if c: ctx.write_kv(layer, int(node), (torch.rand((c, 8, 128), device="cuda")*2-1).bfloat16(), (torch.rand((c, 8, 128), device="cuda")*2-1).bfloat16())
+        if c:
+            ctx.write_kv(layer, int(node), (torch.rand((c, hkv, d), device="cuda") * 2 - 1).bfloat16(),
+                         (torch.rand((c, hkv, d), device="cuda") * 2 - 1).bfloat16())
 L = len(ctx.leaves())
-q = (torch.rand((L, 32, 128), device="cuda")*2-1).bfloat16()
-tr = torch.zeros(512 + 4*4096, dtype=torch.int64, device="cuda")
-ctx.set_option("trace_ptr", tr.data_ptr())
+q = (torch.rand((L, hq, d), device="cuda") * 2 - 1).bfloat16()
 ctx.prepare(128)
-for layer in (0, 1, 0):
+for layer in (0, 1, 0, 1):
     ctx.attend(layer, q)
 torch.cuda.synchronize()
-full = tr.cpu().numpy()
-t = full[:512].reshape(64, 8)
-base = t[0, 0]
-names = ["prod_issue", "qk_data", "qk_issued", "sm_S_seen", "sm_P_pub", "pv_issued", "stage_free"]
-print("cycles rel. to first producer issue; per tile:")
-print("tile " + " ".join(f"{n:>11s}" for n in names))
-for i in range(64):
-    if t[i].any():
-        print(f"{i:4d} " + " ".join(f"{(x - base) if x else 0:11d}" for x in t[i, :7]))
+S = ctx.schedule(128)
+n_cta = S["n_ctas"]
+tr = torch.zeros(n_cta * 256, dtype=torch.int64, device="cuda")
+ctx.set_option("trace_ptr", tr.data_ptr())
+ctx.prepare(128)
+ctx.attend(1, q)
+torch.cuda.synchronize()
+t = tr.cpu().numpy().reshape(n_cta, 256)
+t0 = t[:, 0].min()
+start = (t[:, 0] - t0) / 1e3
+end = (t[:, 1] - t0) / 1e3
+dur = end - start
+print(f"{name}: CTAs {n_cta}, kernel span {end.max():.2f} us, start spread {start.max():.2f} us, "
+      f"dur min/mean/max {dur.min():.2f}/{dur.mean():.2f}/{dur.max():.2f} us")
+for c in list(np.argsort(-dur)[:3]) + list(np.argsort(dur)[:2]):
+    nt = int(t[c, 3])
+    ev = t[c, 8:8 + 8 * 31].reshape(31, 8)
+    b = ev[0, 0]
+    its = [i for i in range(S["cta_begin"][c], S["cta_begin"][c + 1])]
+    desc = [(int(S["items"][i][0]), int(S["items"][i][2] - S["items"][i][1]), int(S["items"][i][4]) * ctx.group)
+            for i in its]
+    print(f"CTA {c} sm {t[c,2]} start {start[c]:.2f} dur {dur[c]:.2f} us tiles {nt} items(head,tiles,rows) {desc}")
+    print("   tile  K_issued    S_seen  S_masked  max_xchg  O_full-1  rescaled     P_pub       epi  (clk rel. first K issue)")
+    for i in range(min(nt, 31)):
+        print("   %4d" % i + "".join(" %9d" % ((x - b) if x else -1) for x in ev[i]))
+    epi = t[c, 248:256]
+    print("   last epilogue: O_full out_stored q_stored tickets merged(mergeA at [6])",
+          " ".join(str((x - b) if x else -1) for x in epi))
 
-c = full[512:].reshape(4096, 4)
-c = c[c[:, 1] > 0]
-t0 = c[:, 0].min()
-dur = (c[:, 1] - c[:, 0]) / 1000.0
-print(f"CTAs {len(c)}  kernel span {(c[:,1].max()-t0)/1000:.1f} us  cta dur mean {dur.mean():.1f} max {dur.max():.1f} us")
-order = np.argsort(-dur)
-print("slowest CTAs: start(us) dur(us) sm groups rows")
-for i in order[:12]:
-    print(f"  {(c[i,0]-t0)/1000:7.1f} {dur[i]:7.1f} {c[i,2]:4d} {c[i,3]>>32:5d} {c[i,3]&0xffffffff:5d}")
-print("dur by rows (live rows -> mean us, mean us per tile):")
-rows = c[:, 3] & 0xffffffff
-grp = c[:, 3] >> 32
-for r in sorted(set(rows.tolist())):
-    m = rows == r
-    print(f"  rows {r:4d}: n={m.sum():4d} dur {dur[m].mean():6.1f} us, per tile {(dur[m] / np.maximum(1, (grp[m]+7)//8)).mean():5.2f} us")
+# phase averages per tile over all CTAs, grouped by the CTA's first item rows
+print("\nper-tile phase means (clk): rows  n_cta  tile_period  S_wait  pass1  xchg  O_wait  rescale  pass2")
+groups = {}
+for c in range(n_cta):
+    nt = min(int(t[c, 3]), 31)
+    if nt < 3:
+        continue
+    ev = t[c, 8:8 + 8 * 31].reshape(31, 8)[:nt].astype(np.float64)
+    i0 = S["cta_begin"][c]
+    rows = int(S["items"][i0][4]) * ctx.group
+    period = np.diff(ev[:, 1]).mean()
+    ph = [(ev[1:, 1] - ev[:-1, 6]).mean()] + [(ev[:, k + 1] - ev[:, k]).mean() for k in range(1, 6)]
+    groups.setdefault(rows, []).append([period] + ph)
+for rows in sorted(groups):
+    v = np.array(groups[rows]).mean(0)
+    print(f"  {rows:4d} {len(groups[rows]):5d} " + " ".join(f"{x:8.0f}" for x in v))
