@@ -105,10 +105,14 @@ def spec_tree(prompt, t_size):
 
 # ------------------------------------------------------------- clocks
 class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms in the
+    background; summary() keeps the samples inside [mark_start, mark_end]."""
+
     def __init__(self, gpu_index=0):
         self.gpu = gpu_index
         self.samples = []
         self._p = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -116,7 +120,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                        "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                        "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except FileNotFoundError:
@@ -125,7 +129,13 @@ class ClockSampler:
 
     def _read(self):
         for line in self._p.stdout:
-            self.samples.append([x.strip() for x in line.split(",")])
+            self.samples.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def __exit__(self, *a):
         if self._p:
@@ -136,18 +146,23 @@ class ClockSampler:
                 self._p.kill()
 
     def summary(self):
-        if not self.samples:
+        smp = self.samples
+        if self.t0 is not None and self.t1 is not None:
+            inside = [x for x in smp if self.t0 <= x[0] <= self.t1]
+            smp = inside or sorted(smp, key=lambda x: abs(x[0] - (self.t0 + self.t1) / 2))[:1]
+        smp = [x[1] for x in smp]
+        if not smp:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in smp if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in smp if len(s) > 1 and s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for s in self.samples:
+        for s in smp:
             for n, v in zip(names, s[3:7]):
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+                "reasons": sorted(reasons), "samples": len(smp)}
 
 
 def measured_peaks():
@@ -209,12 +224,13 @@ def cpu_baseline(cfg, snap, sample_layers=1):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="few_shot", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the layer calls eagerly (no CUDA graph)")
     ap.add_argument("--opt", action="append", default=[], help="ta_set_option key=value (repeatable)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -283,10 +299,32 @@ def main():
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()
 
+    def layers():
+        for layer in range(L_layers):
+            ctx.attend(layer, q[layer], out[layer], stream=torch.cuda.current_stream())
+
+    # one decode step = host plan + schedule + metadata upload (ta_prepare) and
+    # the n_layers attention calls, replayed as a CUDA graph (as a serving
+    # engine captures its decode step; the graph reads the schedule metadata
+    # that ta_prepare re-uploads into the same device buffers every step)
+    ctx.prepare(128, stream)
+    torch.cuda.synchronize()
+    graph = None
+    if not args.no_graph:
+        layers()   # warm the launch configuration before capture
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            layers()
+        torch.cuda.synchronize()
+
     def step():
         ctx.prepare(128, stream)
-        for layer in range(L_layers):
-            ctx.attend(layer, q[layer], out[layer], stream=stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            for layer in range(L_layers):
+                ctx.attend(layer, q[layer], out[layer], stream=stream)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -297,14 +335,18 @@ def main():
     # ---- timed region: device time via CUDA events, max over ranks
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
+        for _ in range(30):   # keep the GPU busy while the sampler starts
+            step()
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+        clocks.mark_start()
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+        clocks.mark_end()
         if world > 1:
             torch.distributed.barrier()
     ms = e0.elapsed_time(e1) / args.steps
@@ -313,18 +355,22 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
 
-    # ---- per-launch timing of the attention kernels (same stream)
-    n_ev = L_layers
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_ev)]
+    # ---- per-layer time of ta_attend (attention + merge launches) on the
+    # launching stream: the graph of n_layers calls, replayed back to back
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx.prepare(128, stream)
     torch.cuda.synchronize()
-    for rep in range(3):
-        for layer in range(L_layers):
-            evs[layer][0].record(stream)
-            ctx.attend(layer, q[layer], out[layer], stream=stream)
-            evs[layer][1].record(stream)
-        torch.cuda.synchronize()
-    attend_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+    reps = 10
+    ev0.record(stream)
+    for _ in range(reps):
+        if graph is not None:
+            graph.replay()
+        else:
+            for layer in range(L_layers):
+                ctx.attend(layer, q[layer], out[layer], stream=stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    attend_ms = ev0.elapsed_time(ev1) / (reps * L_layers)
 
     # ---- e2e through the public host-buffer entry (H2D q + D2H out per layer)
     e2e = None
@@ -395,7 +441,7 @@ def main():
         "partial_io_bytes_per_step": io.partial_bytes * L_layers,
         "meta_bytes_per_step": io.meta_bytes,
         "us_per_layer": attend_ms * 1000.0,
-        "roofline": {"kernel": "ta_attend (attn_fma/attn_mma + merge), per layer", "bound": "hbm",
+        "roofline": {"kernel": "ta_attend (attn_mma or attn_fma + merge), per layer, graph-replayed", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": profile_traffic(args.config),
                      "alg_bytes_per_launch": alg_bytes},

@@ -9,7 +9,7 @@
 //   QK  (warp 1)    S = Q K^T  (M=128, N=16*groups, K=128), Q from TMEM
 //                   -> S buffer (t & 1) in TMEM
 //   PV  (warp 2)    O += P V   (M=128, N=128, K=16*groups), P from TMEM
-//   softmax (warps 4-11, thread = TMEM lane = row, two column halves)
+//   softmax (warps 3-10, thread = TMEM lane = row, two column halves)
 //                   pass 1: tcgen05.ld S -> tree-masked row max; exchange
 //                   with the other half; online softmax in base 2 with lazy
 //                   O rescale; pass 2: tcgen05.ld S -> P = exp2 -> bf16 ->
@@ -45,15 +45,33 @@ constexpr int SMEM_KV = 0;                               // stage s: K at s*STAG
 constexpr int SMEM_BAR = NSTAGE * STAGE;                 // 196608
 constexpr int SMEM_RED = SMEM_BAR + 256;                 // [2 parity][2 half][128] fp32 row max
 constexpr int SMEM_REDL = SMEM_RED + 2 * 2 * BM * 4;     // [2 half][128] fp32 row sum
-constexpr int SMEM_BYTES = SMEM_REDL + 2 * BM * 4 + 1024;   // + alignment slack
-constexpr int NTHREADS = 384;
+// the CTA's schedule, staged once before the dependency wait: items, their
+// tile offsets in the CTA's tile sequence, tile descriptors and metadata
+constexpr int MAXI = 32, MAXT = 112;
+constexpr int SMEM_EPI = SMEM_REDL + 2 * BM * 4;        // [8 warps][32 rows][64 B] epilogue staging
+constexpr int SMEM_ITEM = SMEM_EPI + 8 * 32 * 64;        // ItemDesc[MAXI]
+constexpr int SMEM_IOFF = SMEM_ITEM + MAXI * 32;         // int[MAXI + 1]
+constexpr int SMEM_TD = SMEM_IOFF + 256;                 // TileDesc[MAXT]
+constexpr int SMEM_TM = SMEM_TD + MAXT * 16;             // TileMeta[MAXT]
+constexpr int MAXS = 512;                                // staged slot leaves
+constexpr int SMEM_SOFF = SMEM_TM + MAXT * 64;           // int[MAXI + 1]: item -> offset into s_slot
+constexpr int SMEM_SLOT = SMEM_SOFF + 256;               // int[MAXS]
+constexpr int SMEM_BYTES = SMEM_SLOT + MAXS * 4 + 1024;  // + alignment slack
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+constexpr int NTHREADS = 352;                           // 3 issuer warps + 8 softmax warps
+constexpr int SOFT0 = 3;                                 // first softmax warp
+constexpr int TRACE_TID = SOFT0 * 32;                    // thread that records the softmax trace
 constexpr int NSOFT = 256;
 constexpr int TMEM_COLS = 512;
-constexpr int TMEM_S = 0, TMEM_O = 256, TMEM_P = 384, TMEM_Q = 448;
+constexpr int TMEM_S = 0, TMEM_O = 256, TMEM_Q = 384;   // S0, S1 (P aliased), O, Q0, Q1 (item parity)
 constexpr float kLazy = 8.0f;                            // rescale O only when the max grows by > 2^8
 
-enum { FULLK = 0, FULLV = 3, EMPTYK = 6, EMPTYV = 9, S_FULL = 12, S_FREE = 14, P_FULL = 16, O_FULL = 17, Q_FULL = 18,
-       Q_FREE = 19, NBAR = 20 };
+// Per-tile barriers are double-buffered by tile parity (S_FULL, S_FREE,
+// P_FULL, O_FULL): the softmax warps may run one tile ahead of the PV
+// issuer, and a waiter must never be two phases behind its barrier.
+enum { FULLK = 0, FULLV = 3, EMPTYK = 6, EMPTYV = 9, S_FULL = 12, S_FREE = 14, P_FULL = 16, O_FULL = 18, Q_FULL = 20,
+       Q_FREE = 22, NBAR = 24 };
+static_assert(NBAR * 8 <= 192, "barriers overlap the TMEM slot");
 
 // Optional pipeline trace (debug; AttnArgs::trace != nullptr): per CTA 256
 // int64 slots: [0] start / [1] end (%globaltimer ns), [2] SM id, [3] tiles,
@@ -67,9 +85,13 @@ __device__ __forceinline__ long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define TA_TRACE_EPI(a, k)                                                                         \
+// epilogue phases: slots 240.. for the CTA's first item, 248.. for its last
+#define TA_TRACE_EPI(a, item, k)                                                                   \
     do {                                                                                           \
-        if ((a).trace && threadIdx.x == 128) (a).trace[blockIdx.x * TRACE_SLOTS + 248 + (k)] = clock64(); \
+        if ((a).trace && threadIdx.x == TRACE_TID) {                                               \
+            if ((item) == 0) (a).trace[blockIdx.x * TRACE_SLOTS + 240 + (k)] = clock64();          \
+            (a).trace[blockIdx.x * TRACE_SLOTS + 248 + (k)] = clock64();                           \
+        }                                                                                          \
     } while (0)
 #define TA_TRACE(a, t, k)                                                                          \
     do {                                                                                           \
@@ -94,18 +116,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int it0 = a.cta_begin[blockIdx.x], it1 = a.cta_begin[blockIdx.x + 1];
+    const int n_items = it1 - it0;
+    ItemDesc* s_item = reinterpret_cast<ItemDesc*>(smem + SMEM_ITEM);
+    int* s_ioff = reinterpret_cast<int*>(smem + SMEM_IOFF);
+    TileDesc* s_td = reinterpret_cast<TileDesc*>(smem + SMEM_TD);
+    TileMeta* s_tm = reinterpret_cast<TileMeta*>(smem + SMEM_TM);
+    int* s_soff = reinterpret_cast<int*>(smem + SMEM_SOFF);
+    int* s_slot = reinterpret_cast<int*>(smem + SMEM_SLOT);
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2 * NSTAGE; ++i) mbar_init(BAR(FULLK + i), 1);       // FULLK, FULLV
         for (int i = 0; i < 2 * NSTAGE; ++i) mbar_init(BAR(EMPTYK + i), 1);      // EMPTYK, EMPTYV
         for (int i = 0; i < 2; ++i) {
             mbar_init(BAR(S_FULL + i), 1);
-            mbar_init(BAR(S_FREE + i), NSOFT);
+            mbar_init(BAR(S_FREE + i), 1);
+            mbar_init(BAR(P_FULL + i), NSOFT);
+            mbar_init(BAR(O_FULL + i), 1);
         }
-        mbar_init(BAR(P_FULL), NSOFT);
-        mbar_init(BAR(O_FULL), 1);
-        mbar_init(BAR(Q_FULL), NSOFT);
-        mbar_init(BAR(Q_FREE), 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(BAR(Q_FULL + i), NSOFT);
+            mbar_init(BAR(Q_FREE + i), 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
@@ -121,9 +152,40 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             prefetch_tmap(&tm.v[i]);
         }
     }
+    // stage this CTA's schedule (written by the host before the launch, so it
+    // is read before the dependency wait, overlapping the previous launch)
+    const int ni_s = min(n_items, MAXI);
+    for (int k = threadIdx.x; k < ni_s; k += NTHREADS) s_item[k] = a.items[it0 + k];
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (threadIdx.x == 0) {
+        int off = 0, soff = 0;
+        for (int k = 0; k < ni_s; ++k) {
+            s_ioff[k] = off;
+            off += s_item[k].tile_end - s_item[k].tile_begin;
+            s_soff[k] = soff;
+            soff += s_item[k].n_slots;
+        }
+        s_ioff[ni_s] = off;
+        s_soff[ni_s] = soff;
+    }
+    __syncthreads();
+    const int ns_s = min(s_soff[ni_s], MAXS);    // staged slot leaves
+    for (int x = threadIdx.x; x < ns_s; x += NTHREADS) {
+        int k = 0;
+        while (s_soff[k + 1] <= x) ++k;
+        s_slot[x] = a.slot_leaf[s_item[k].slot_begin + x - s_soff[k]];
+    }
+    const int nt_s = min(s_ioff[ni_s], MAXT);   // staged tiles: CTA tile index < nt_s
+    for (int x = threadIdx.x; x < nt_s; x += NTHREADS) {
+        int k = 0;
+        while (s_ioff[k + 1] <= x) ++k;
+        const int t = s_item[k].tile_begin + x - s_ioff[k];
+        s_td[x] = a.tiles[t];
+        s_tm[x] = a.tile_meta[t];
+    }
+    __syncthreads();
     const uint32_t tmem = *tmem_slot;
     pdl_launch_dependents();
     pdl_wait();   // previous launch finished: queries, outputs, partial scratch are ours
@@ -133,89 +195,60 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
         a.trace[blockIdx.x * TRACE_SLOTS + 2] = smid;
     }
-
-    // next tile of this CTA after tile t of item ii (-1: none); *nii = its item
-    auto next_tile = [&](int ii, int t, int tile_end, int* nii) -> int {
-        if (t + 1 < tile_end) {
-            *nii = ii;
-            return t + 1;
-        }
-        *nii = ii + 1;
-        return ii + 1 < it1 ? a.items[ii + 1].tile_begin : -1;
+    // schedule accessors: k = CTA-local item index, lt = CTA-local tile index
+    auto item_at = [&](int k) -> ItemDesc { return k < MAXI ? s_item[k] : a.items[it0 + k]; };
+    auto td_at = [&](int lt, int t) -> TileDesc { return lt < nt_s ? s_td[lt] : a.tiles[t]; };
+    auto tm_at = [&](int lt, int t) -> const TileMeta* { return lt < nt_s ? &s_tm[lt] : &a.tile_meta[t]; };
+    auto leaf_at = [&](int k, const ItemDesc& I, int jj) -> int {   // leaf of slot jj of item k
+        return (k < ni_s && s_soff[k] + jj < ns_s) ? s_slot[s_soff[k] + jj] : a.slot_leaf[I.slot_begin + jj];
     };
 
     if (warp == 0) {
         // ===================== TMA producer =====================
-        if (lane == 0 && it0 < it1) {
-            int gt = 0, ii = it0;
-            ItemDesc I = a.items[ii];
-            int t = I.tile_begin;
-            TileDesc td = a.tiles[t];
-            int4 rlo = *reinterpret_cast<const int4*>(a.tile_meta[t].row);
-            int4 rhi = *reinterpret_cast<const int4*>(a.tile_meta[t].row + 4);
-            while (true) {
-                // prefetch the next tile's descriptor and rows (independent loads)
-                int nii;
-                const int nt = next_tile(ii, t, I.tile_end, &nii);
-                TileDesc ntd{};
-                int4 nrlo{}, nrhi{};
-                if (nt >= 0) {
-                    ntd = a.tiles[nt];
-                    nrlo = *reinterpret_cast<const int4*>(a.tile_meta[nt].row);
-                    nrhi = *reinterpret_cast<const int4*>(a.tile_meta[nt].row + 4);
-                }
-                const int rows8[8] = {rlo.x, rlo.y, rlo.z, rlo.w, rhi.x, rhi.y, rhi.z, rhi.w};
-                auto row_of = [&](int g) {   // register select (no local-memory indexing)
-                    int v = rows8[0];
-#pragma unroll
-                    for (int k = 1; k < 8; ++k) v = g == k ? rows8[k] : v;
-                    return v;
-                };
+        if (lane > 0) fill_empty(a, lane - 1, 31);
+        if (lane == 0) {
+            int gt = 0;
+            for (int k = 0; k < n_items; ++k) {
+                const ItemDesc I = item_at(k);
                 const int64_t row0 = a.layer_row0 + (int64_t)I.head * a.head_rows;
-                const int s = gt % NSTAGE;
-                const uint32_t ph = (uint32_t)(gt / NSTAGE) & 1u;
-                const uint32_t kdst = sbase + SMEM_KV + (uint32_t)s * STAGE;
-                const uint32_t vdst = kdst + TILE;
-                const uint32_t bytes = (uint32_t)td.ng * 4096u;
-                mbar_wait(BAR(EMPTYK + s), ph ^ 1);
-                mbar_expect_tx(BAR(FULLK + s), bytes);
-                for (int b = 0; b < td.nbox; ++b) {
-                    const int g = td.box[b] >> 2, sz = td.box[b] & 3;
-                    const int row = (int)(row0 + row_of(g));
-                    tma_load_2d(kdst + g * 2048, &tm.k[sz], 0, row, BAR(FULLK + s));
-                    tma_load_2d(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s));
+                for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
+                    const TileDesc td = td_at(gt, t);
+                    const TileMeta* tmp = tm_at(gt, t);
+                    const int s = gt % NSTAGE;
+                    const uint32_t ph = (uint32_t)(gt / NSTAGE) & 1u;
+                    const uint32_t kdst = sbase + SMEM_KV + (uint32_t)s * STAGE;
+                    const uint32_t vdst = kdst + TILE;
+                    const uint32_t bytes = (uint32_t)td.ng * 4096u;
+                    mbar_wait(BAR(EMPTYK + s), ph ^ 1);
+                    mbar_expect_tx(BAR(FULLK + s), bytes);
+                    for (int b = 0; b < td.nbox; ++b) {
+                        const int g = td.box[b] >> 2, sz = td.box[b] & 3;
+                        const int row = (int)(row0 + tmp->row[g]);
+                        tma_load_2d(kdst + g * 2048, &tm.k[sz], 0, row, BAR(FULLK + s));
+                        tma_load_2d(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s));
+                    }
+                    TA_TRACE(a, gt, 0);
+                    mbar_wait(BAR(EMPTYV + s), ph ^ 1);
+                    mbar_expect_tx(BAR(FULLV + s), bytes);
+                    for (int b = 0; b < td.nbox; ++b) {
+                        const int g = td.box[b] >> 2, sz = td.box[b] & 3;
+                        const int row = (int)(row0 + tmp->row[g]);
+                        tma_load_2d(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + s));
+                        tma_load_2d(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + s));
+                    }
                 }
-                TA_TRACE(a, gt, 0);
-                mbar_wait(BAR(EMPTYV + s), ph ^ 1);
-                mbar_expect_tx(BAR(FULLV + s), bytes);
-                for (int b = 0; b < td.nbox; ++b) {
-                    const int g = td.box[b] >> 2, sz = td.box[b] & 3;
-                    const int row = (int)(row0 + row_of(g));
-                    tma_load_2d(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + s));
-                    tma_load_2d(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + s));
-                }
-                ++gt;
-                if (nt < 0) break;
-                if (nii != ii) {
-                    ii = nii;
-                    I = a.items[ii];
-                }
-                t = nt;
-                td = ntd;
-                rlo = nrlo;
-                rhi = nrhi;
             }
         }
     } else if (warp == 1) {
         // ===================== QK issuer: S = Q K^T =====================
         if (lane == 0) {
             int gt = 0;
-            for (int ii = it0; ii < it1; ++ii) {
-                const ItemDesc I = a.items[ii];
-                int ng = a.tiles[I.tile_begin].ng;
-                mbar_wait(BAR(Q_FULL), (ii - it0) & 1);
+            for (int k = 0; k < n_items; ++k) {
+                const ItemDesc I = item_at(k);
+                const int qb = k & 1;   // Q buffer of this item
+                mbar_wait(BAR(Q_FULL + qb), (k >> 1) & 1);
                 for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
-                    const int ng_next = t + 1 < I.tile_end ? a.tiles[t + 1].ng : 0;
+                    const int ng = td_at(gt, t).ng;
                     const int s = gt % NSTAGE, sb = gt & 1;
                     mbar_wait(BAR(FULLK + s), (uint32_t)(gt / NSTAGE) & 1u);
                     if (gt >= 2) mbar_wait(BAR(S_FREE + sb), ((gt >> 1) - 1) & 1);
@@ -223,103 +256,116 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const uint32_t sK = sbase + SMEM_KV + (uint32_t)s * STAGE;
                     const uint32_t id = idesc_bf16(BM, 16 * ng, 0, 0);
 #pragma unroll
-                    for (int k = 0; k < DH / 16; ++k) {
-                        const uint32_t off = (uint32_t)((k >> 2) * HALF + (k & 3) * 32);
-                        mma_bf16_ts(tmem + TMEM_S + sb * 128, tmem + TMEM_Q + 8 * k, sdesc(sK + off, 16, 1024), id, k > 0);
+                    for (int kq = 0; kq < DH / 16; ++kq) {
+                        const uint32_t off = (uint32_t)((kq >> 2) * HALF + (kq & 3) * 32);
+                        mma_bf16_ts(tmem + TMEM_S + sb * 128, tmem + TMEM_Q + 64 * qb + 8 * kq, sdesc(sK + off, 16, 1024), id,
+                                    kq > 0);
                     }
                     mma_commit(BAR(S_FULL + sb));
                     mma_commit(BAR(EMPTYK + s));
-                    ng = ng_next;
                 }
-                mma_commit(BAR(Q_FREE));
+                mma_commit(BAR(Q_FREE + qb));
             }
         }
     } else if (warp == 2) {
         // ===================== PV issuer: O += P V =====================
         if (lane == 0) {
             int gt = 0;
-            for (int ii = it0; ii < it1; ++ii) {
-                const ItemDesc I = a.items[ii];
-                int ng = a.tiles[I.tile_begin].ng;
+            for (int k = 0; k < n_items; ++k) {
+                const ItemDesc I = item_at(k);
                 for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
-                    const int ng_next = t + 1 < I.tile_end ? a.tiles[t + 1].ng : 0;
+                    const int ng = td_at(gt, t).ng;
                     const int s = gt % NSTAGE;
+                    const int sb = gt & 1;
                     mbar_wait(BAR(FULLV + s), (uint32_t)(gt / NSTAGE) & 1u);
-                    mbar_wait(BAR(P_FULL), gt & 1);
+                    mbar_wait(BAR(P_FULL + sb), (gt >> 1) & 1);
                     tc_fence_after();
                     const uint32_t sV = sbase + SMEM_KV + (uint32_t)s * STAGE + TILE;
                     const uint32_t id = idesc_bf16(BM, DH, 0, 1);
                     const bool first = t == I.tile_begin;
+                    // P of group kk: bf16 pairs in columns [16kk, 16kk+8) of S buffer sb
                     for (int kk = 0; kk < ng; ++kk)
-                        mma_bf16_ts(tmem + TMEM_O, tmem + TMEM_P + 8 * kk, sdesc(sV + kk * 2048, HALF, 1024), id,
-                                    (!first || kk > 0) ? 1u : 0u);
+                        mma_bf16_ts(tmem + TMEM_O, tmem + TMEM_S + sb * 128 + 16 * kk, sdesc(sV + kk * 2048, HALF, 1024),
+                                    id, (!first || kk > 0) ? 1u : 0u);
                     mma_commit(BAR(EMPTYV + s));
-                    mma_commit(BAR(O_FULL));
-                    ng = ng_next;
+                    mma_commit(BAR(S_FREE + sb));
+                    mma_commit(BAR(O_FULL + sb));
                 }
             }
         }
-    } else if (warp == 3) {
-        fill_empty(a, lane);
     } else {
         // ===================== softmax / epilogue (256 threads) =====================
-        const int q4 = warp & 3;                 // TMEM lane quadrant of this warp
-        const int h = (warp - 4) >> 2;           // column half (S groups 4h..4h+3, O / Q columns 64h..)
+        const int q4 = warp & 3;                 // TMEM lane quadrant of this warp (warps 3..10)
+        const int h = (warp - SOFT0) >> 2;       // column half (S groups 4h..4h+3, O / Q columns 64h..)
         const int r = q4 * 32 + lane;            // row == TMEM lane
         const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
         const int G = a.G;
         const float sc = a.scale_log2;
 
-        // Q rows of item ii (this thread: dims [64h, 64h+64) of row r, i.e.
-        // 32 packed bf16 pairs): global loads into registers, then (once the
-        // previous item's QK is complete) tcgen05.st into the Q columns
-        auto q_fetch = [&](int ii, uint4 (&v)[8]) {
-            const ItemDesc I = a.items[ii];
-            if (r < I.n_slots * G) {
-                const int leaf = a.slot_leaf[I.slot_begin + r / G];
-                const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.q) +
-                                                                  ((size_t)leaf * a.hq_loc + I.head * G + r % G) * DH);
+        // Q row of an item (this thread: dims [64h, 64h+64) of row r = 32
+        // packed bf16 pairs) -> registers -> (once the previous item's QK is
+        // complete) tcgen05.st into the Q columns
+        auto q_row = [&](const ItemDesc& I, int leaf) -> const uint4* {
+            return reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.q) +
+                                                  ((size_t)leaf * a.hq_loc + I.head * G + r % G) * DH) + 8 * h;
+        };
+        auto q_fetch = [&](const ItemDesc& I, int leaf, uint4 (&v)[8]) {
+            if (leaf >= 0) {
+                const uint4* src = q_row(I, leaf);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) v[c] = src[8 * h + c];
+                for (int c = 0; c < 8; ++c) v[c] = src[c];
             } else {
 #pragma unroll
                 for (int c = 0; c < 8; ++c) v[c] = make_uint4(0, 0, 0, 0);
             }
         };
-        auto q_store = [&](const uint4 (&v)[8]) {
+        auto q_store = [&](const uint4 (&v)[8], int qb) {
             const uint32_t* w = reinterpret_cast<const uint32_t*>(v);
-            TA_TMEM_ST16(tmem + lane_addr + TMEM_Q + 32 * h, w);
-            TA_TMEM_ST16(tmem + lane_addr + TMEM_Q + 32 * h + 16, (w + 16));
+            TA_TMEM_ST16(tmem + lane_addr + TMEM_Q + 64 * qb + 32 * h, w);
+            TA_TMEM_ST16(tmem + lane_addr + TMEM_Q + 64 * qb + 32 * h + 16, (w + 16));
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(BAR(Q_FULL));
+            mbar_arrive(BAR(Q_FULL + qb));
         };
 
-        if (it0 < it1) {
+        if (n_items > 0) {
+            const ItemDesc I0 = item_at(0);
             uint4 qv[8];
-            q_fetch(it0, qv);
-            q_store(qv);
+            q_fetch(I0, r < I0.n_slots * G ? leaf_at(0, I0, r / G) : -1, qv);
+            q_store(qv, 0);
         }
         int gt = 0;
-        for (int ii = it0; ii < it1; ++ii) {
-            const ItemDesc I = a.items[ii];
+        for (int k = 0; k < n_items; ++k) {
+            const ItemDesc I = item_at(k);
             const int nrows = I.n_slots * G;
             const bool live_row = r < nrows;
             const int j = live_row ? r / G : 0;      // local query slot
             const int g_in = r % G;
             const bool warp_live = q4 * 32 < nrows;
             float m = -INFINITY, l = 0.f;
-            // this thread's half of the tile metadata, prefetched a tile ahead
-            TileDesc td = a.tiles[I.tile_begin];
-            uint4 inf = *reinterpret_cast<const uint4*>(a.tile_meta[I.tile_begin].info + 4 * h);
+            // this row's output code; the next item's Q goes to the other Q
+            // buffer during this item's first tile (L2-prefetched before it)
+            const bool has_next = k + 1 < n_items;
+            const int code = live_row ? a.slot_out[I.out_begin + j] : kSlotUnused;
+            if ((a.debug & 4) && code != kSlotUnused) {
+                // warm L2 with the lines this row's epilogue writes (no fill under load)
+                const char* dst = code >= 0 ? reinterpret_cast<const char*>(a.part_o + ((size_t)code * G + g_in) * DH + 64 * h)
+                                            : reinterpret_cast<const char*>(a.out) +
+                                                  (((size_t)(-1 - code) * a.hq_loc + I.head * G + g_in) * DH + 64 * h) *
+                                                      (a.out_bf16 ? 2 : 4);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(dst));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(dst + 128));
+            }
+            int nleaf = -1;
+            if (has_next) {
+                const ItemDesc In = item_at(k + 1);
+                nleaf = r < In.n_slots * G ? leaf_at(k + 1, In, r / G) : -1;
+                if (nleaf >= 0 && !(a.debug & 2)) asm volatile("prefetch.global.L2 [%0];" ::"l"(q_row(In, nleaf)));
+            }
 
             for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
-                TileDesc ntd{};
-                uint4 ninf{};
-                if (t + 1 < I.tile_end) {
-                    ntd = a.tiles[t + 1];
-                    ninf = *reinterpret_cast<const uint4*>(a.tile_meta[t + 1].info + 4 * h);
-                }
+                const TileDesc td = td_at(gt, t);
+                const uint4 inf = *reinterpret_cast<const uint4*>(tm_at(gt, t)->info + 4 * h);
                 const int ng = td.ng;
                 const int g0 = 4 * h;
                 const uint32_t info[4] = {inf.x, inf.y, inf.z, inf.w};
@@ -336,35 +382,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int sb = gt & 1;
                 const uint32_t s_addr = tmem + lane_addr + TMEM_S + sb * 128;
                 mbar_wait(BAR(S_FULL + sb), (gt >> 1) & 1);
-                if (threadIdx.x == 128) TA_TRACE(a, gt, 1);
+                if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 1);
                 tc_fence_after();
-                // pass 1: masked row max of my half (scale > 0 commutes with max)
+                // S of my half into registers (one pass), tree mask, row max
+                uint32_t r0[16], r1[16], r2[16], r3[16];
                 float mx = -INFINITY;
                 if (warp_att) {
+                    // groups past ng hold stale columns; lim == 0 masks them
+                    TA_TMEM_LD16(s_addr + g0 * 16, r0);
+                    TA_TMEM_LD16(s_addr + (g0 + 1) * 16, r1);
+                    TA_TMEM_LD16(s_addr + (g0 + 2) * 16, r2);
+                    TA_TMEM_LD16(s_addr + (g0 + 3) * 16, r3);
+                    tmem_wait_ld();
 #pragma unroll
-                    for (int g2 = 0; g2 < 4; g2 += 2) {
-                        if (g0 + g2 < ng) {
-                            uint32_t rr[32];
-                            TA_TMEM_LD16(s_addr + (g0 + g2) * 16, rr);
-                            if (g0 + g2 + 1 < ng) TA_TMEM_LD16(s_addr + (g0 + g2 + 1) * 16, (rr + 16));
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int c = 0; c < 16; ++c) {
-                                if (c < lim[g2]) mx = fmaxf(mx, __uint_as_float(rr[c]));
-                                if (c < lim[g2 + 1]) mx = fmaxf(mx, __uint_as_float(rr[16 + c]));
-                            }
-                        }
+                    for (int c = 0; c < 16; ++c) {
+                        r0[c] = c < lim[0] ? r0[c] : 0xff800000u;   // -inf
+                        r1[c] = c < lim[1] ? r1[c] : 0xff800000u;
+                        r2[c] = c < lim[2] ? r2[c] : 0xff800000u;
+                        r3[c] = c < lim[3] ? r3[c] : 0xff800000u;
+                        mx = fmaxf(fmaxf(mx, fmaxf(__uint_as_float(r0[c]), __uint_as_float(r1[c]))),
+                                   fmaxf(__uint_as_float(r2[c]), __uint_as_float(r3[c])));
                     }
                 }
-                if (threadIdx.x == 128) TA_TRACE(a, gt, 2);
+                if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 2);
                 // combine the two column halves of the row (partner warp: same quadrant)
                 float* rd = red + (gt & 1) * 2 * BM;
                 rd[h * BM + r] = mx;
                 named_bar(1 + q4, 64);
                 mx = fmaxf(mx, rd[(h ^ 1) * BM + r]) * sc;
-                if (threadIdx.x == 128) TA_TRACE(a, gt, 3);
+                if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 3);
                 // lazy rescale: keep the stale max unless it grew by > kLazy (both
-                // threads of a row decide alike).  The O correction is warp-collective.
+                // threads of a row decide alike).  The O correction is warp-collective
+                // and the only reason to wait for PV(t-1) here.
                 const bool grow = mx > m + kLazy;
                 float f = 1.f;
                 if (grow) {
@@ -372,10 +421,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     l *= f;
                     m = mx;
                 }
-                if (gt > 0) mbar_wait(BAR(O_FULL), (gt - 1) & 1);   // PV(t-1) done: P free, O settled
-                if (threadIdx.x == 128) TA_TRACE(a, gt, 4);
-                tc_fence_after();
                 if (t > I.tile_begin && __any_sync(0xffffffffu, grow && f != 1.f)) {
+                    mbar_wait(BAR(O_FULL + (sb ^ 1)), ((gt - 1) >> 1) & 1);   // PV(t-1) done
+                    tc_fence_after();
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         uint32_t o[16];
@@ -386,89 +434,119 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         TA_TMEM_ST16(tmem + lane_addr + TMEM_O + h * 64 + c * 16, o);
                     }
                 }
-                if (threadIdx.x == 128) TA_TRACE(a, gt, 5);
+                if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 5);
                 if (warp_att) {
-                    // pass 2: P = exp2(s * scale - m) -> bf16 pairs -> TMEM; l += sum(P)
+                    // P = exp2(s * scale - m) -> bf16 pairs -> S columns [16g, 16g+8); l += sum(P)
                     const float negm = m == -INFINITY ? 0.f : -m;
                     float la = 0.f;
+                    auto emit = [&](const uint32_t (&rv)[16], int g) {
+                        uint32_t pk[8];
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        if (g0 + g < ng) {
-                            uint32_t rr[16];
-                            TA_TMEM_LD16(s_addr + (g0 + g) * 16, rr);
-                            tmem_wait_ld();
-                            uint32_t pk[8];
-#pragma unroll
-                            for (int c = 0; c < 8; ++c) {
-                                const float p0 = 2 * c < lim[g] ? ex2(fmaf(__uint_as_float(rr[2 * c]), sc, negm)) : 0.f;
-                                const float p1 =
-                                    2 * c + 1 < lim[g] ? ex2(fmaf(__uint_as_float(rr[2 * c + 1]), sc, negm)) : 0.f;
-                                la += p0 + p1;
-                                pk[c] = pack_bf16(p0, p1);
-                            }
-                            TA_TMEM_ST8(tmem + lane_addr + TMEM_P + 8 * (g0 + g), pk);
+                        for (int c = 0; c < 8; ++c) {
+                            const float p0 = ex2(fmaf(__uint_as_float(rv[2 * c]), sc, negm));
+                            const float p1 = ex2(fmaf(__uint_as_float(rv[2 * c + 1]), sc, negm));
+                            la += p0 + p1;
+                            pk[c] = pack_bf16(p0, p1);
                         }
-                    }
+                        TA_TMEM_ST8(s_addr + 16 * (g0 + g), pk);
+                    };
+                    // P past ng lands in S columns PV never reads
+                    emit(r0, 0);
+                    emit(r1, 1);
+                    emit(r2, 2);
+                    emit(r3, 3);
                     l += la;
                 } else if (warp_live) {
                     // no row of this warp attends my half of the tile: P = 0
                     const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
                     for (int g = 0; g < 4; ++g)
-                        if (g0 + g < ng) TA_TMEM_ST8(tmem + lane_addr + TMEM_P + 8 * (g0 + g), z);
+                        if (g0 + g < ng) TA_TMEM_ST8(s_addr + 16 * (g0 + g), z);
                 }
                 tmem_wait_st();
                 tc_fence_before();
-                mbar_arrive(BAR(S_FREE + sb));
-                mbar_arrive(BAR(P_FULL));
-                if (threadIdx.x == 128) TA_TRACE(a, gt, 6);
-                td = ntd;
-                inf = ninf;
+                mbar_arrive(BAR(P_FULL + sb));
+                if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 6);
+                if (has_next && t == I.tile_begin) {
+                    // next item's Q -> the other Q buffer (free once item k-1's QK is done)
+                    uint4 qv[8];
+                    q_fetch(item_at(k + 1), nleaf, qv);
+                    if (k >= 1) mbar_wait(BAR(Q_FREE + ((k + 1) & 1)), ((k - 1) >> 1) & 1);
+                    tc_fence_after();
+                    q_store(qv, (k + 1) & 1);
+                }
             }
 
-            // ---- epilogue.  Next item's Q: global loads now, TMEM after O is out
-            const bool has_next = ii + 1 < it1;
-            uint4 qv[8];
-            if (has_next) q_fetch(ii + 1, qv);
-            mbar_wait(BAR(O_FULL), (gt - 1) & 1);
-            TA_TRACE_EPI(a, 0);
+            // ---- epilogue
+            mbar_wait(BAR(O_FULL + ((gt - 1) & 1)), ((gt - 1) >> 1) & 1);   // PV(last) and all before it
+            TA_TRACE_EPI(a, k, 0);
             tc_fence_after();
+            TA_TRACE_EPI(a, k, 1);
             redl[h * BM + r] = l;
             named_bar(1 + q4, 64);
             l += redl[(h ^ 1) * BM + r];
             const float inv = l > 0.f ? 1.f / l : 0.f;
             const float lse2 = m + log2f(l);
-            const int code = live_row ? a.slot_out[I.out_begin + j] : kSlotUnused;
-            const int hq = I.head * G + g_in;
+            if (code != kSlotUnused && h == 0) {
+                if (code < 0) {
+                    if (a.lse) a.lse[(size_t)(-1 - code) * a.hq_loc + I.head * G + g_in] = lse2 * kLn2;
+                } else {
+                    a.part_lse[(size_t)code * G + g_in] = lse2;
+                }
+            }
             if (warp_live) {
+                // O / l -> final output or partial record, 16 columns at a time:
+                // row-wise into this warp's SMEM staging (chunks swizzled by
+                // (row >> 1) & 3: conflict-free both ways), then every store
+                // instruction writes 8 rows x 64 contiguous bytes.  Compact
+                // loops: this code runs once per item, I-cache cold.
+                const uint32_t epi = sbase + SMEM_EPI + (uint32_t)(warp - SOFT0) * 2048;
+                int dcode[4];
 #pragma unroll
+                for (int s4 = 0; s4 < 4; ++s4) dcode[s4] = __shfl_sync(0xffffffffu, code, 8 * s4 + (lane >> 2));
+                TA_TRACE_EPI(a, k, 3);
+#pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     uint32_t o[16];
                     const int col = h * 64 + c * 16;
                     TA_TMEM_LD16(tmem + lane_addr + TMEM_O + col, o);
                     tmem_wait_ld();
-                    if (code != kSlotUnused) {
-                        const float* of = reinterpret_cast<const float*>(o);
-                        if (code < 0) {
-                            const int leaf = -1 - code;
-                            store_row<16>(a.out, ((size_t)leaf * a.hq_loc + hq) * DH + col, of, inv, a.out_bf16);
-                            if (c == 0 && h == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = lse2 * kLn2;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        sts128(epi + (uint32_t)(lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)),
+                               __float_as_uint(__uint_as_float(o[4 * q]) * inv),
+                               __float_as_uint(__uint_as_float(o[4 * q + 1]) * inv),
+                               __float_as_uint(__uint_as_float(o[4 * q + 2]) * inv),
+                               __float_as_uint(__uint_as_float(o[4 * q + 3]) * inv));
+                    __syncwarp();
+#pragma unroll
+                    for (int s4 = 0; s4 < 4; ++s4) {
+                        const int rl = 8 * s4 + (lane >> 2), ch = lane & 3;   // staged row, 16-byte chunk
+                        const int cd = dcode[s4];
+                        float4 v;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                                     : "r"(epi + (uint32_t)(rl * 64 + ((ch ^ ((rl >> 1) & 3)) << 4)))
+                                     : "memory");
+                        if (cd == kSlotUnused || (a.debug & 1)) continue;
+                        const int gq = (q4 * 32 + rl) % G, c0 = col + 4 * ch;
+                        if (cd < 0) {
+                            const size_t o_ = ((size_t)(-1 - cd) * a.hq_loc + I.head * G + gq) * DH + c0;
+                            if (a.out_bf16)
+                                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + o_) =
+                                    make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+                            else
+                                *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + o_) = v;
                         } else {
-                            store_row<16>(a.part_o, ((size_t)code * G + g_in) * DH + col, of, inv, 0);
-                            if (c == 0 && h == 0) a.part_lse[(size_t)code * G + g_in] = lse2;
+                            *reinterpret_cast<float4*>(a.part_o + ((size_t)cd * G + gq) * DH + c0) = v;
                         }
                     }
+                    __syncwarp();
                 }
             }
-            TA_TRACE_EPI(a, 1);
-            if (has_next) {
-                mbar_wait(BAR(Q_FREE), (ii - it0) & 1);
-                tc_fence_after();
-                q_store(qv);
-            } else {
-                tc_fence_before();
-            }
-            if (threadIdx.x == 128) TA_TRACE(a, gt - 1, 7);
+            TA_TRACE_EPI(a, k, 2);
+            tc_fence_before();
+            if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt - 1, 7);
         }
     }
 
@@ -477,7 +555,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS + 1] = gtimer();
         int nt = 0;
-        for (int ii = it0; ii < it1; ++ii) nt += a.items[ii].tile_end - a.items[ii].tile_begin;
+        for (int k = 0; k < n_items; ++k) nt += item_at(k).tile_end - item_at(k).tile_begin;
         a.trace[blockIdx.x * TRACE_SLOTS + 3] = nt;
     }
     if (warp == 1) {

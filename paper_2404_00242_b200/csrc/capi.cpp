@@ -66,6 +66,7 @@ struct ta_ctx {
     const int32_t* d_empty = nullptr;
     bool pdl = true;
     int64_t trace = 0;  // debug: device buffer for the MMA kernel's pipeline trace
+    int debug = 0;      // debug experiment bits
     int num_sms = 148;
 
     // host copy of the schedule for ta_schedule_get
@@ -245,6 +246,12 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
         } else if (k == "tile_cost") {
             if (v < 0) fail(TA_ERR_INVALID_ARGUMENT, "tile_cost must be >= 0");
             c->opt.tile_cost = (int)v;
+        } else if (k == "row_cost") {
+            if (v < 0) fail(TA_ERR_INVALID_ARGUMENT, "row_cost must be >= 0");
+            c->opt.row_cost = (int)v;
+        } else if (k == "item_cost") {
+            if (v < 0) fail(TA_ERR_INVALID_ARGUMENT, "item_cost must be >= 0");
+            c->opt.item_cost = (int)v;
         } else if (k == "num_ctas") {
             if (v < 1 || v > 65535) fail(TA_ERR_INVALID_ARGUMENT, "num_ctas must be in [1, 65535]");
             c->opt.num_ctas = (int)v;
@@ -254,6 +261,8 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->pdl = v != 0;
         } else if (k == "trace_ptr") {
             c->trace = v;
+        } else if (k == "debug") {
+            c->debug = (int)v;
         } else {
             fail(TA_ERR_INVALID_ARGUMENT, "unknown option " + k);
         }
@@ -560,6 +569,7 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.kv_bf16 = c->shape.kv_dtype == TA_BF16;
     a.out_bf16 = c->shape.out_dtype == TA_BF16;
     a.trace = reinterpret_cast<long long*>(c->trace);
+    a.debug = c->debug;
     const SchedOptions o = effective_opts(c);
     if (o.use_mma)
         cuda_check(launch_attn_mma(a, c->pdl, s), "attn_mma");

@@ -576,21 +576,25 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
         }
     }
 
-    // ---- 3. CTA runs over the (head, lane, tile) sequence
+    // ---- 3. CTA runs over the (head, lane, tile) sequence.  Cost of a tile:
+    // its box rows (bytes) + a fixed per-tile cost + a softmax cost growing
+    // with the lane's rows; every item a CTA starts costs item_cost more.
     const int n_tiles = (int)S.tiles.size();
+    std::vector<int32_t> tile_lane(n_tiles);
+    for (int li = 0; li < (int)lanes.size(); ++li)
+        for (int i = lanes[li].tile_begin; i < lanes[li].tile_end; ++i) tile_lane[i] = li;
     std::vector<int64_t> tcost(n_tiles);
-    int64_t per_head = 0;
+    int64_t per_head = (int64_t)opt.item_cost * (int64_t)lanes.size();
     for (int i = 0; i < n_tiles; ++i) {
-        tcost[i] = 16LL * S.tiles[i].ng + opt.tile_cost;
+        const int rows = lanes[tile_lane[i]].n_slots * G;
+        tcost[i] = 16LL * S.tiles[i].ng + opt.tile_cost + (int64_t)opt.row_cost * rows / 128;
         per_head += tcost[i];
         S.kv_rows_loaded += 16LL * S.tiles[i].ng * n_heads;
     }
     const int n_cta = std::max(1, opt.num_ctas);
-    const int64_t total = per_head * n_heads;
+    // each CTA boundary opens one more item than the (head, lane) count
+    const int64_t total = per_head * n_heads + (int64_t)opt.item_cost * (n_cta - 1);
     S.cta_begin.assign(1, 0);
-    std::vector<int32_t> tile_lane(n_tiles);
-    for (int li = 0; li < (int)lanes.size(); ++li)
-        for (int i = lanes[li].tile_begin; i < lanes[li].tile_end; ++i) tile_lane[i] = li;
     {
         int cta = 0;
         int64_t acc = 0;
@@ -614,6 +618,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                     it.n_slots = lanes[li].n_slots;
                     S.items.push_back(it);
                     open = &S.items.back();
+                    acc += opt.item_cost;
                 }
                 open->tile_end = i + 1;
                 acc += tcost[i];

@@ -52,6 +52,7 @@ struct AttnArgs {
     int kv_bf16;
     int out_bf16;
     long long* trace;         // optional clock64 trace (debug)
+    int debug;                // debug experiment bits (0 in production)
 };
 
 // tcgen05/TMEM path (bf16, D = 128).

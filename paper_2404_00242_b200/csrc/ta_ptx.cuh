@@ -139,19 +139,20 @@ __device__ __forceinline__ void store_row(void* out, size_t base, const float* v
 }
 
 // Leaf-heads whose path holds no tokens: out = 0, lse = -inf (they are
-// absent from the reference's AttentionOutput).  One warp, strided over CTAs.
-__device__ __forceinline__ void fill_empty(const AttnArgs& a, int lane) {
+// absent from the reference's AttentionOutput).  `nl` lanes (ids 0..nl-1) of
+// one warp, strided over CTAs.
+__device__ __forceinline__ void fill_empty(const AttnArgs& a, int lane, int nl = 32) {
     for (int e = blockIdx.x; e < a.n_empty; e += gridDim.x) {
         const int leaf = a.empty[2 * e], head = a.empty[2 * e + 1];
         const size_t base = ((size_t)leaf * a.hq_loc + (size_t)head * a.G) * a.D;
-        for (int i = lane; i < a.G * a.D; i += 32) {
+        for (int i = lane; i < a.G * a.D; i += nl) {
             if (a.out_bf16)
                 reinterpret_cast<__nv_bfloat16*>(a.out)[base + i] = __float2bfloat16_rn(0.f);
             else
                 reinterpret_cast<float*>(a.out)[base + i] = 0.f;
         }
         if (a.lse)
-            for (int g = lane; g < a.G; g += 32) a.lse[(size_t)leaf * a.hq_loc + head * a.G + g] = -INFINITY;
+            for (int g = lane; g < a.G; g += nl) a.lse[(size_t)leaf * a.hq_loc + head * a.G + g] = -INFINITY;
     }
 }
 

@@ -15,7 +15,7 @@ while read id; do
     [ -z "$first" ] && first="$id"
   fi
 done < gpurun_out/gpu_ids.txt
-if [ -n "$first" ]; then
+if [ -n "$first" ] && [ -n "$SANITIZE" ]; then
   timeout 600 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest "$first" -q -x -p no:cacheprovider > gpurun_out/sanitizer.log 2>&1
   grep -E "Invalid|misaligned|at 0x|by thread|Address" gpurun_out/sanitizer.log | head -40
 fi

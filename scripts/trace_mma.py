@@ -64,9 +64,10 @@ for c in list(np.argsort(-dur)[:3]) + list(np.argsort(dur)[:2]):
     print("   tile  K_issued    S_seen  S_masked  max_xchg  O_full-1  rescaled     P_pub       epi  (clk rel. first K issue)")
     for i in range(min(nt, 31)):
         print("   %4d" % i + "".join(" %9d" % ((x - b) if x else -1) for x in ev[i]))
-    epi = t[c, 248:256]
-    print("   last epilogue: O_full out_stored q_stored tickets merged(mergeA at [6])",
-          " ".join(str((x - b) if x else -1) for x in epi))
+    for nm, sl in (("first", 240), ("last", 248)):
+        epi = t[c, sl:sl + 4]
+        print(f"   {nm} item epilogue: O_full_seen  l_xchg_start  O_loaded  stored:",
+              " ".join(str((x - b) if x else -1) for x in epi))
 
 # phase averages per tile over all CTAs, grouped by the CTA's first item rows
 print("\nper-tile phase means (clk): rows  n_cta  tile_period  S_wait  pass1  xchg  O_wait  rescale  pass2")
