@@ -59,10 +59,7 @@ struct ta_ctx {
     const int32_t* d_cta_begin = nullptr;
     const int32_t* d_slot_leaf = nullptr;
     const int32_t* d_slot_out = nullptr;
-    const int32_t* d_merge_head = nullptr;
-    const int32_t* d_merge_leaf = nullptr;
-    const int32_t* d_merge_begin = nullptr;
-    const int32_t* d_merge_parts = nullptr;
+    const int4* d_merge_rec = nullptr;
     const int32_t* d_empty = nullptr;
     bool pdl = true;
     int64_t trace = 0;  // debug: device buffer for the MMA kernel's pipeline trace
@@ -478,10 +475,10 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             {S.cta_begin.data(), S.cta_begin.size() * 4, 0},
             {S.slot_leaf.data(), S.slot_leaf.size() * 4, 0},
             {S.slot_out.data(), S.slot_out.size() * 4, 0},
-            {S.merge_head.data(), S.merge_head.size() * 4, 0},
-            {S.merge_leaf.data(), S.merge_leaf.size() * 4, 0},
-            {S.merge_begin.data(), S.merge_begin.size() * 4, 0},
-            {S.merge_parts.data(), S.merge_parts.size() * 4, 0},
+            {S.merge_rec.data(), S.merge_rec.size() * 16, 0},
+            {nullptr, 0, 0},
+            {nullptr, 0, 0},
+            {nullptr, 0, 0},
             {S.empty.data(), S.empty.size() * 4, 0},
         };
         size_t total = 0;
@@ -508,10 +505,7 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         c->d_cta_begin = (const int32_t*)(d + parts[5].off);
         c->d_slot_leaf = (const int32_t*)(d + parts[6].off);
         c->d_slot_out = (const int32_t*)(d + parts[7].off);
-        c->d_merge_head = (const int32_t*)(d + parts[8].off);
-        c->d_merge_leaf = (const int32_t*)(d + parts[9].off);
-        c->d_merge_begin = (const int32_t*)(d + parts[10].off);
-        c->d_merge_parts = (const int32_t*)(d + parts[11].off);
+        c->d_merge_rec = (const int4*)(d + parts[8].off);
         c->d_empty = (const int32_t*)(d + parts[12].off);
         // partial scratch: o [n_part][G][D] + lse [n_part][G]
         const size_t pf = (size_t)std::max(1, S.n_partials) * c->G * (c->shape.d_head + 1);
@@ -555,10 +549,7 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.cta_begin = c->d_cta_begin;
     a.slot_leaf = c->d_slot_leaf;
     a.slot_out = c->d_slot_out;
-    a.merge_leaf = c->d_merge_leaf;
-    a.merge_head = c->d_merge_head;
-    a.merge_begin = c->d_merge_begin;
-    a.merge_parts = c->d_merge_parts;
+    a.merge_rec = c->d_merge_rec;
     a.empty = c->d_empty;
     a.n_empty = (int)(S.empty.size() / 2);
     a.n_ctas = (int)S.cta_begin.size() - 1;
@@ -623,8 +614,7 @@ ta_status ta_io_stats_get(ta_ctx* c, ta_io_stats* o) {
         o->meta_bytes = (int64_t)(S.tiles.size() * (sizeof(TileDesc) + sizeof(TileMeta)) +
                                   S.items.size() * sizeof(ItemDesc)) +
                         (int64_t)(S.grp_row.size() + S.grp_info.size() + S.cta_begin.size() + S.slot_leaf.size() +
-                                  S.slot_out.size() + S.merge_head.size() + S.merge_leaf.size() +
-                                  S.merge_begin.size() + S.merge_parts.size() + S.empty.size()) * 4;
+                                  S.slot_out.size() + 4 * S.merge_rec.size() + S.empty.size()) * 4;
         o->flops = S.masked_q_tokens * c->hq_loc * 4 * D;
     });
 }

@@ -650,8 +650,11 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
             }
         }
     }
+    // partial ids are contiguous per merge record (record mi owns ids
+    // [merge_begin[mi], merge_begin[mi+1]) in item order), so the merge reads
+    // them without an id list
     std::vector<int32_t> rec((size_t)L * n_heads, -1);  // leaf-head -> merge record
-    std::vector<std::vector<int32_t>> rec_parts;
+    std::vector<std::vector<int32_t*>> rec_codes;
     for (const ItemDesc& it : S.items) {
         for (int j = 0; j < it.n_slots; ++j) {
             int32_t& code = S.slot_out[it.out_begin + j];
@@ -663,24 +666,27 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                 continue;
             }
             if (rec[key] < 0) {
-                rec[key] = (int32_t)rec_parts.size();
-                rec_parts.emplace_back();
+                rec[key] = (int32_t)rec_codes.size();
+                rec_codes.emplace_back();
                 S.merge_leaf.push_back(leaf);
                 S.merge_head.push_back(it.head);
             }
-            code = S.n_partials++;
-            S.part_merge.push_back(rec[key]);
-            rec_parts[rec[key]].push_back(code);
+            rec_codes[rec[key]].push_back(&code);
         }
+    }
+    S.merge_begin.assign(1, 0);
+    for (std::size_t mi = 0; mi < rec_codes.size(); ++mi) {
+        for (int32_t* c : rec_codes[mi]) {
+            *c = S.n_partials++;
+            S.part_merge.push_back((int32_t)mi);
+            S.merge_parts.push_back(*c);
+        }
+        S.merge_begin.push_back(S.n_partials);
+        S.merge_rec.push_back({S.merge_leaf[mi], S.merge_head[mi], S.merge_begin[mi], S.n_partials - S.merge_begin[mi]});
     }
     for (ItemDesc& it : S.items)
         for (int j = 0; j < it.n_slots; ++j)
             if (S.slot_out[it.out_begin + j] >= 0) it.pad |= 1;   // holds partials: takes part in merges
-    S.merge_begin.assign(1, 0);
-    for (const auto& v : rec_parts) {
-        S.merge_parts.insert(S.merge_parts.end(), v.begin(), v.end());
-        S.merge_begin.push_back((int32_t)S.merge_parts.size());
-    }
     for (int32_t l = 0; l < L; ++l)
         for (int h = 0; h < n_heads; ++h)
             if (cover[(size_t)l * n_heads + h] == 0) {

@@ -2,13 +2,13 @@
 //
 // Runs right after the attention launch of a layer (programmatic dependent
 // launch: its CTAs start as the attention CTAs retire and wait for their
-// memory).  One warp per (leaf-head merge record, q head in the group):
-// lane k fetches partial k's id and log2-lse (all in flight at once), the
-// weights 2^(lse_k - M) / sum are broadcast by shuffle, and every lane sums
-// its D/32 columns over the partials with independent loads.  Partials are
-// consumed in the schedule's fixed (item) order, so the result does not
-// depend on CTA timing.  The partial records were written by the attention
-// launch moments earlier and are read from L2.
+// memory).  One warp per (leaf-head merge record, q head in the group).  A
+// record's partial ids are contiguous, so after the one 16-byte record load
+// (read before the dependency wait) every partial's log2-lse (lane k:
+// partial k) and every partial's columns (lane: D/32 columns of each) are
+// loaded at once -- one memory round trip after the wait.  Partials are combined in the schedule's fixed (item)
+// order, so the result does not depend on CTA timing.  The records were
+// written moments earlier and are read from L2.
 #include "ta_ptx.cuh"
 
 namespace ta {
@@ -29,30 +29,40 @@ __device__ __forceinline__ void ld_cols(const float* p, float (&f)[DPL]) {
     }
 }
 
+constexpr int PB = 8;   // partials loaded per batch (all in flight together)
+
 template <int DPL>
-__global__ void __launch_bounds__(256) merge_kernel(const AttnArgs a, int n_merge) {
+__global__ void __launch_bounds__(128) merge_kernel(const AttnArgs a, int n_merge) {
     pdl_launch_dependents();
-    pdl_wait();   // the attention launch's partials are complete
-    const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int wid = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (wid >= n_merge * a.G) return;
-    const int mi = wid / a.G, g = wid % a.G;
-    const int leaf = a.merge_leaf[mi];
-    const int pb = a.merge_begin[mi], pe = a.merge_begin[mi + 1];
-    const int D = a.D;
-    const int hq = a.merge_head[mi] * a.G + g;
+    const bool live = wid < n_merge * a.G;
+    const int mi = live ? wid / a.G : 0, g = wid % a.G;
+    // the record is host-written schedule metadata: read it before the wait
+    const int4 rec = live ? __ldg(a.merge_rec + mi) : make_int4(0, 0, 0, 0);   // leaf, head, first partial, count
+    pdl_wait();   // the attention launch's partials are complete
+    if (!live) return;
+    const int D = a.D, G = a.G;
+    const int hq = rec.y * G + g;
     const bool active = lane * DPL < D;
     float acc[DPL];
 #pragma unroll
     for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
     float M = -INFINITY, den = 0.f;
-    for (int base = pb; base < pe; base += 32) {
-        const int np = min(32, pe - base);
-        int pid = 0;
-        float lp = -INFINITY;
-        if (lane < np) {
-            pid = a.merge_parts[base + lane];
-            lp = __ldcg(a.part_lse + (size_t)pid * a.G + g);
+    for (int base = 0; base < rec.w; base += 32) {
+        const int np = min(32, rec.w - base);
+        const int p0 = rec.z + base;
+        // this chunk's lse (lane k) and the first batch of columns, together
+        const float lp = lane < np ? __ldcg(a.part_lse + (size_t)(p0 + lane) * G + g) : -INFINITY;
+        float v[PB][DPL];
+#pragma unroll
+        for (int u = 0; u < PB; ++u) {
+            if (active && u < np) {
+                ld_cols<DPL>(a.part_o + ((size_t)(p0 + u) * G + g) * D + lane * DPL, v[u]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < DPL; ++i) v[u][i] = 0.f;
+            }
         }
         float bm = lp;
 #pragma unroll
@@ -69,39 +79,39 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnArgs a, int n_merg
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, off);
         den += ws;
-        for (int p = 0; p < np; p += 8) {
-            float v[8][DPL];
-            float wv[8];
+        for (int p = 0; p < np; p += PB) {
+            if (p > 0) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int id = __shfl_sync(0xffffffffu, pid, (p + u) & 31);
-                wv[u] = p + u < np ? __shfl_sync(0xffffffffu, w, (p + u) & 31) : 0.f;
-                if (active && p + u < np) {
-                    ld_cols<DPL>(a.part_o + ((size_t)id * a.G + g) * D + lane * DPL, v[u]);
-                } else {
+                for (int u = 0; u < PB; ++u) {
+                    if (active && p + u < np) {
+                        ld_cols<DPL>(a.part_o + ((size_t)(p0 + p + u) * G + g) * D + lane * DPL, v[u]);
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < DPL; ++i) v[u][i] = 0.f;
+                        for (int i = 0; i < DPL; ++i) v[u][i] = 0.f;
+                    }
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < PB; ++u) {
+                const float wu = __shfl_sync(0xffffffffu, w, (p + u) & 31);
 #pragma unroll
-                for (int i = 0; i < DPL; ++i) acc[i] = fmaf(wv[u], v[u][i], acc[i]);
+                for (int i = 0; i < DPL; ++i) acc[i] = fmaf(p + u < np ? wu : 0.f, v[u][i], acc[i]);
+            }
         }
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;
-    const size_t base = ((size_t)leaf * a.hq_loc + hq) * D;
+    const size_t ob = ((size_t)rec.x * a.hq_loc + hq) * D;
     if (active) {
 #pragma unroll
         for (int i = 0; i < DPL; ++i) {
-            const size_t o = base + lane * DPL + i;
+            const size_t o = ob + lane * DPL + i;
             if (a.out_bf16)
                 reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(acc[i] * inv);
             else
                 reinterpret_cast<float*>(a.out)[o] = acc[i] * inv;
         }
     }
-    if (lane == 0 && a.lse) a.lse[(size_t)leaf * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
+    if (lane == 0 && a.lse) a.lse[(size_t)rec.x * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
 }
 
 }  // namespace
@@ -109,8 +119,8 @@ __global__ void __launch_bounds__(256) merge_kernel(const AttnArgs a, int n_merg
 cudaError_t launch_merge(const AttnArgs& a, int n_merge, bool pdl, cudaStream_t s) {
     if (n_merge == 0) return cudaSuccess;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((n_merge * a.G + 7) / 8);
-    cfg.blockDim = dim3(256);
+    cfg.gridDim = dim3((n_merge * a.G + 3) / 4);
+    cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

@@ -185,7 +185,11 @@ struct Schedule {
     std::vector<int32_t> part_merge;  // partial id -> merge record
     std::vector<int32_t> merge_leaf, merge_head;  // merge record -> leaf index, local kv head
     std::vector<int32_t> merge_begin; // [n_merge + 1] into merge_parts
-    std::vector<int32_t> merge_parts; // partial ids in merge order (item order)
+    std::vector<int32_t> merge_parts; // partial ids in merge order (item order; contiguous per record)
+    struct MergeRec {
+        int32_t leaf, head, pbegin, n;
+    };
+    std::vector<MergeRec> merge_rec;  // device copy: one 16-byte load per record
     std::vector<int32_t> empty;       // [n][2] (leaf, local head) pairs with no path tokens
     int32_t n_lanes = 0;
     int32_t n_partials = 0;

@@ -38,10 +38,7 @@ struct AttnArgs {
     const int32_t* cta_begin;
     const int32_t* slot_leaf;
     const int32_t* slot_out;
-    const int32_t* merge_leaf;
-    const int32_t* merge_head;
-    const int32_t* merge_begin;
-    const int32_t* merge_parts;
+    const int4* merge_rec;    // [n_merge] {leaf, local kv head, first partial id, count}
     const int32_t* empty;     // [n_empty][2] (leaf, head)
     int n_empty;
     int n_ctas;
