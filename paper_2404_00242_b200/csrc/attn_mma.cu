@@ -188,6 +188,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
     const uint32_t tmem = *tmem_slot;
     pdl_launch_dependents();
+    // warm L2 with the first tiles' KV and the first item's query rows while
+    // the previous launch drains (prefetches carry no ordering obligations)
+    if (warp == 0 && lane < NSTAGE && lane < nt_s && !(a.debug & 8)) {
+        int k = 0;
+        while (s_ioff[k + 1] <= lane) ++k;
+        const int64_t row0 = a.layer_row0 + (int64_t)s_item[k].head * a.head_rows;
+        const TileDesc td = s_td[lane];
+        for (int b = 0; b < td.nbox; ++b) {
+            const int g = td.box[b] >> 2, sz = td.box[b] & 3;
+            const int row = (int)(row0 + s_tm[lane].row[g]);
+            tma_prefetch_2d(&tm.k[sz], 0, row);
+            tma_prefetch_2d(&tm.k[sz], 64, row);
+            tma_prefetch_2d(&tm.v[sz], 0, row);
+            tma_prefetch_2d(&tm.v[sz], 64, row);
+        }
+    }
+    if (warp >= SOFT0 && n_items > 0 && !(a.debug & 8)) {
+        const int r = (warp & 3) * 32 + lane, h = (warp - SOFT0) >> 2;
+        const ItemDesc I0 = s_item[0];
+        if (r < I0.n_slots * a.G && r / a.G < ns_s) {
+            const __nv_bfloat16* qp = reinterpret_cast<const __nv_bfloat16*>(a.q) +
+                                      ((size_t)s_slot[r / a.G] * a.hq_loc + I0.head * a.G + r % a.G) * DH + 64 * h;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(qp));
+        }
+    }
     pdl_wait();   // previous launch finished: queries, outputs, partial scratch are ours
     if (a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS] = gtimer();
