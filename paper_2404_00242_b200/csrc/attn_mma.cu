@@ -69,9 +69,12 @@ constexpr float kLazy = 8.0f;                            // rescale O only when 
 // Per-tile barriers are double-buffered by tile parity (S_FULL, S_FREE,
 // P_FULL, O_FULL): the softmax warps may run one tile ahead of the PV
 // issuer, and a waiter must never be two phases behind its barrier.
+// ITEM_DONE / ITEM_ACK: the softmax warps' partial stores of item k are
+// published (release) by helper lanes of warp 2 (in-kernel merge only).
 enum { FULLK = 0, FULLV = 3, EMPTYK = 6, EMPTYV = 9, S_FULL = 12, S_FREE = 14, P_FULL = 16, O_FULL = 18, Q_FULL = 20,
-       Q_FREE = 22, NBAR = 24 };
-static_assert(NBAR * 8 <= 192, "barriers overlap the TMEM slot");
+       Q_FREE = 22, ITEM_DONE = 24, ITEM_ACK = 26, NBAR = 28 };
+constexpr int TMEM_SLOT = 240;                           // offset of the TMEM address in the barrier block
+static_assert(NBAR * 8 <= TMEM_SLOT, "barriers overlap the TMEM slot");
 
 // Optional pipeline trace (debug; AttnArgs::trace != nullptr): per CTA 256
 // int64 slots: [0] start / [1] end (%globaltimer ns), [2] SM id, [3] tiles,
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar0 = sbase + SMEM_BAR;
     auto BAR = [&](int i) { return bar0 + 8u * (uint32_t)i; };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM_BAR + 192);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM_BAR + TMEM_SLOT);
     float* red = reinterpret_cast<float*>(smem + SMEM_RED);
     float* redl = reinterpret_cast<float*>(smem + SMEM_REDL);
 
@@ -136,6 +139,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int i = 0; i < 2; ++i) {
             mbar_init(BAR(Q_FULL + i), NSOFT);
             mbar_init(BAR(Q_FREE + i), 1);
+            mbar_init(BAR(ITEM_DONE + i), NSOFT);
+            mbar_init(BAR(ITEM_ACK + i), 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
@@ -316,6 +321,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mma_commit(BAR(S_FREE + sb));
                     mma_commit(BAR(O_FULL + sb));
                 }
+            }
+        } else if (a.inline_merge) {
+            // lanes 1..31: publish each item's partial records.  The softmax
+            // warps' stores are ordered before ITEM_DONE (mbarrier release);
+            // a gpu-scope fence here makes them visible before the arrival
+            // count of each record is bumped (merged by whichever CTA waits).
+            for (int k = 0; k < n_items; ++k) {
+                const ItemDesc I = item_at(k);
+                mbar_wait(BAR(ITEM_DONE + (k & 1)), (k >> 1) & 1);
+                if (I.pad & 1) {
+                    __threadfence();
+                    for (int jj = lane - 1; jj < I.n_slots; jj += 31) {
+                        const int cd = a.slot_out[I.out_begin + jj];
+                        if (cd >= 0) atomicAdd(a.merge_sync + 1 + a.part_merge[cd], 1);
+                    }
+                }
+                __syncwarp(0xfffffffeu);
+                if (lane == 1) mbar_arrive(BAR(ITEM_ACK + (k & 1)));
             }
         }
     } else {
@@ -571,7 +594,44 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             TA_TRACE_EPI(a, k, 2);
             tc_fence_before();
+            if (a.inline_merge) {
+                if (k >= 2) mbar_wait(BAR(ITEM_ACK + (k & 1)), ((k - 2) >> 1) & 1);
+                mbar_arrive(BAR(ITEM_DONE + (k & 1)));
+            }
             if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt - 1, 7);
+        }
+
+        if (a.inline_merge) {
+            // ---- merge (tree_reduce): every softmax warp of every CTA takes
+            // records off a global queue and merges each once all its partials
+            // have arrived.  All CTAs are resident, so the wait always ends.
+            const int total = (int)gridDim.x * 8;
+            const int n_task = a.n_merge * G;            // one task per (record, q head)
+            while (true) {
+                int tid_ = 0;
+                if (lane == 0) tid_ = atomicAdd(a.merge_sync, 1);
+                tid_ = __shfl_sync(0xffffffffu, tid_, 0);
+                if (tid_ >= n_task) {
+                    if (lane == 0 && tid_ == n_task + total - 1) a.merge_sync[0] = 0;   // last grab resets
+                    break;
+                }
+                const int rid = tid_ / G, g = tid_ % G;
+                const int4 rec = __ldg(a.merge_rec + rid);
+                if (lane == 0) {
+                    while (true) {
+                        int v;
+                        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.merge_sync + 1 + rid) : "memory");
+                        if (v >= rec.w) break;
+                        __nanosleep(a.debug >> 8);
+                    }
+                }
+                __syncwarp();
+                __threadfence();   // every lane: acquire side of the partials it reads
+                merge_record_row<4>(a, rec, g, lane);
+                // the record's last task to finish resets its arrival count
+                __syncwarp();
+                if (lane == 0 && atomicAdd(a.merge_sync + 1 + rid, 1) == rec.w + G - 1) a.merge_sync[1 + rid] = 0;
+            }
         }
     }
 

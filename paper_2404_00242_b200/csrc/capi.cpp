@@ -60,8 +60,12 @@ struct ta_ctx {
     const int32_t* d_slot_leaf = nullptr;
     const int32_t* d_slot_out = nullptr;
     const int4* d_merge_rec = nullptr;
+    const int32_t* d_part_merge = nullptr;
+    int* merge_sync = nullptr;      // in-kernel merge queue + arrival counters (self-resetting)
+    size_t merge_sync_cap = 0;      // bytes
     const int32_t* d_empty = nullptr;
     bool pdl = true;
+    bool inline_merge = false;   // measured slower than the PDL-chained merge launch
     int64_t trace = 0;  // debug: device buffer for the MMA kernel's pipeline trace
     int debug = 0;      // debug experiment bits
     int num_sms = 148;
@@ -89,6 +93,7 @@ struct ta_ctx {
             cudaFree(meta_dev);
             cudaFreeHost(meta_host);
             cudaFree(part);
+            cudaFree(merge_sync);
             cudaFree(stage_dev);
             cudaFreeHost(stage_host);
             cudaFree(io_dev);
@@ -256,6 +261,8 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->opt.final_direct = v != 0;
         } else if (k == "pdl") {
             c->pdl = v != 0;
+        } else if (k == "inline_merge") {
+            c->inline_merge = v != 0;
         } else if (k == "trace_ptr") {
             c->trace = v;
         } else if (k == "debug") {
@@ -476,7 +483,7 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             {S.slot_leaf.data(), S.slot_leaf.size() * 4, 0},
             {S.slot_out.data(), S.slot_out.size() * 4, 0},
             {S.merge_rec.data(), S.merge_rec.size() * 16, 0},
-            {nullptr, 0, 0},
+            {S.part_merge.data(), S.part_merge.size() * 4, 0},
             {nullptr, 0, 0},
             {nullptr, 0, 0},
             {S.empty.data(), S.empty.size() * 4, 0},
@@ -506,6 +513,7 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         c->d_slot_leaf = (const int32_t*)(d + parts[6].off);
         c->d_slot_out = (const int32_t*)(d + parts[7].off);
         c->d_merge_rec = (const int4*)(d + parts[8].off);
+        c->d_part_merge = (const int32_t*)(d + parts[9].off);
         c->d_empty = (const int32_t*)(d + parts[12].off);
         // partial scratch: o [n_part][G][D] + lse [n_part][G]
         const size_t pf = (size_t)std::max(1, S.n_partials) * c->G * (c->shape.d_head + 1);
@@ -515,6 +523,15 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             grow_dev(&p, &cap, pf * sizeof(float));
             c->part = (float*)p;
             c->part_cap = cap / sizeof(float);
+        }
+        const size_t ms = (S.merge_rec.size() + 1) * sizeof(int);
+        if (ms > c->merge_sync_cap) {
+            // earlier launches may still use the old counters
+            cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+            void* p = c->merge_sync;
+            grow_dev(&p, &c->merge_sync_cap, ms);
+            c->merge_sync = (int*)p;
+            cuda_check(cudaMemset(c->merge_sync, 0, c->merge_sync_cap), "cudaMemset(merge_sync)");
         }
         c->prepared = true;
         c->prepared_version = c->tree.version;
@@ -550,6 +567,9 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.slot_leaf = c->d_slot_leaf;
     a.slot_out = c->d_slot_out;
     a.merge_rec = c->d_merge_rec;
+    a.part_merge = c->d_part_merge;
+    a.merge_sync = c->merge_sync;
+    a.n_merge = (int)S.merge_rec.size();
     a.empty = c->d_empty;
     a.n_empty = (int)(S.empty.size() / 2);
     a.n_ctas = (int)S.cta_begin.size() - 1;
@@ -562,11 +582,14 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.trace = reinterpret_cast<long long*>(c->trace);
     a.debug = c->debug;
     const SchedOptions o = effective_opts(c);
+    // merge inside the attention launch when every CTA is resident at once
+    // (the merging CTAs wait on the producing ones); else a merge launch
+    a.inline_merge = o.use_mma && c->inline_merge && a.n_ctas <= c->num_sms ? 1 : 0;
     if (o.use_mma)
         cuda_check(launch_attn_mma(a, c->pdl, s), "attn_mma");
     else
         cuda_check(launch_attn_fma(a, o.fma_max_rows, c->pdl, s), "attn_fma");
-    cuda_check(launch_merge(a, (int)S.merge_leaf.size(), c->pdl, s), "merge");
+    if (!a.inline_merge) cuda_check(launch_merge(a, a.n_merge, c->pdl, s), "merge");
 }
 
 ta_status ta_attend(ta_ctx* c, int layer, const void* q, void* out, float* lse, void* stream) {
@@ -655,7 +678,9 @@ ta_status ta_schedule_get(ta_ctx* c, int bs, ta_schedule_view* o) {
 
 int ta_launches_per_attend(ta_ctx* c) {
     if (!c || !c->prepared) return 0;
-    return 1 + (c->sched.merge_leaf.empty() ? 0 : 1);
+    const SchedOptions o = effective_opts(c);
+    const bool inl = o.use_mma && c->inline_merge && (int)c->sched.cta_begin.size() - 1 <= c->num_sms;
+    return 1 + (c->sched.merge_leaf.empty() || inl ? 0 : 1);
 }
 
 }  // extern "C"

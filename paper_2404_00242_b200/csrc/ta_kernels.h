@@ -39,6 +39,10 @@ struct AttnArgs {
     const int32_t* slot_leaf;
     const int32_t* slot_out;
     const int4* merge_rec;    // [n_merge] {leaf, local kv head, first partial id, count}
+    const int32_t* part_merge;// partial id -> merge record
+    int* merge_sync;          // [0] record queue, [1 + mi] arrivals of record mi (self-resetting)
+    int n_merge;
+    int inline_merge;         // merge inside the attention launch (all CTAs co-resident)
     const int32_t* empty;     // [n_empty][2] (leaf, head)
     int n_empty;
     int n_ctas;

@@ -142,6 +142,103 @@ __device__ __forceinline__ void store_row(void* out, size_t base, const float* v
     }
 }
 
+// tree_reduce (attention.hpp:209-233) of one merge record row (q head g of
+// the record's leaf-head) by one warp: lane k < n holds partial k's log2-lse,
+// every lane sums its DPL columns over the partials (ids rec.z .. rec.z +
+// rec.w - 1, contiguous), 8 partials' loads in flight at a time.  Fixed
+// order: the result does not depend on which CTA produced what when.
+template <int DPL>
+__device__ __forceinline__ void ldcg_cols(const float* p, float (&f)[DPL]) {
+    if constexpr (DPL == 4) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(p));
+        f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+    } else if constexpr (DPL == 2) {
+        const float2 v = __ldcg(reinterpret_cast<const float2*>(p));
+        f[0] = v.x; f[1] = v.y;
+    } else {
+        f[0] = __ldcg(p);
+    }
+}
+
+template <int DPL>
+__device__ __forceinline__ void merge_record_row(const AttnArgs& a, int4 rec, int g, int lane) {
+    constexpr int PB = 8;
+    const int D = a.D, G = a.G;
+    const int hq = rec.y * G + g;
+    const bool active = lane * DPL < D;
+    float acc[DPL];
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
+    float M = -INFINITY, den = 0.f;
+    for (int base = 0; base < rec.w; base += 32) {
+        const int np = min(32, rec.w - base);
+        const int p0 = rec.z + base;
+        const float lp = lane < np ? __ldcg(a.part_lse + (size_t)(p0 + lane) * G + g) : -INFINITY;
+        float v[PB][DPL];
+#pragma unroll
+        for (int u = 0; u < PB; ++u) {
+            if (active && u < np) {
+                ldcg_cols<DPL>(a.part_o + ((size_t)(p0 + u) * G + g) * D + lane * DPL, v[u]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < DPL; ++i) v[u][i] = 0.f;
+            }
+        }
+        float bm = lp;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, off));
+        if (bm == -INFINITY) continue;
+        const float nm = fmaxf(M, bm);
+        const float rescale = M == -INFINITY ? 0.f : ex2(M - nm);
+        den *= rescale;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) acc[i] *= rescale;
+        M = nm;
+        const float w = lp == -INFINITY ? 0.f : ex2(lp - M);
+        float ws = w;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, off);
+        den += ws;
+        for (int p = 0; p < np; p += PB) {
+            if (p > 0) {
+#pragma unroll
+                for (int u = 0; u < PB; ++u) {
+                    if (active && p + u < np) {
+                        ldcg_cols<DPL>(a.part_o + ((size_t)(p0 + p + u) * G + g) * D + lane * DPL, v[u]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < DPL; ++i) v[u][i] = 0.f;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < PB; ++u) {
+                const float wu = __shfl_sync(0xffffffffu, w, (p + u) & 31);
+#pragma unroll
+                for (int i = 0; i < DPL; ++i) acc[i] = fmaf(p + u < np ? wu : 0.f, v[u][i], acc[i]);
+            }
+        }
+    }
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    const size_t ob = ((size_t)rec.x * a.hq_loc + hq) * D;
+    if (active) {
+        if (a.out_bf16) {
+            if constexpr (DPL == 4) {
+                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + ob + lane * 4) =
+                    make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
+            } else {
+#pragma unroll
+                for (int i = 0; i < DPL; ++i)
+                    reinterpret_cast<__nv_bfloat16*>(a.out)[ob + lane * DPL + i] = __float2bfloat16_rn(acc[i] * inv);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < DPL; ++i) reinterpret_cast<float*>(a.out)[ob + lane * DPL + i] = acc[i] * inv;
+        }
+    }
+    if (lane == 0 && a.lse) a.lse[(size_t)rec.x * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
+}
+
 // Leaf-heads whose path holds no tokens: out = 0, lse = -inf (they are
 // absent from the reference's AttentionOutput).  `nl` lanes (ids 0..nl-1) of
 // one warp, strided over CTAs.
