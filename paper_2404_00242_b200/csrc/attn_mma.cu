@@ -106,7 +106,7 @@ struct TmapSet {
     CUtensorMap v[4];
 };
 
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __maxnreg__(160)
     attn_mma_kernel(const __grid_constant__ TmapSet tm, const AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     pdl_launch_dependents();
     // warm L2 with the first tiles' KV and the first item's query rows while
     // the previous launch drains (prefetches carry no ordering obligations)
-    if (warp == 0 && lane < NSTAGE && lane < nt_s && !(a.debug & 8)) {
+    if (warp == 0 && lane < a.prefetch_tiles && lane < nt_s) {
         int k = 0;
         while (s_ioff[k + 1] <= lane) ++k;
         const int64_t row0 = a.layer_row0 + (int64_t)s_item[k].head * a.head_rows;

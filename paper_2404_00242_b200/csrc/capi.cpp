@@ -65,6 +65,7 @@ struct ta_ctx {
     size_t merge_sync_cap = 0;      // bytes
     const int32_t* d_empty = nullptr;
     bool pdl = true;
+    int prefetch_tiles = 3;
     bool inline_merge = false;   // measured slower than the PDL-chained merge launch
     int64_t trace = 0;  // debug: device buffer for the MMA kernel's pipeline trace
     int debug = 0;      // debug experiment bits
@@ -261,6 +262,9 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->opt.final_direct = v != 0;
         } else if (k == "pdl") {
             c->pdl = v != 0;
+        } else if (k == "prefetch_tiles") {
+            if (v < 0 || v > 32) fail(TA_ERR_INVALID_ARGUMENT, "prefetch_tiles must be in [0, 32]");
+            c->prefetch_tiles = (int)v;
         } else if (k == "inline_merge") {
             c->inline_merge = v != 0;
         } else if (k == "trace_ptr") {
@@ -581,6 +585,7 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.out_bf16 = c->shape.out_dtype == TA_BF16;
     a.trace = reinterpret_cast<long long*>(c->trace);
     a.debug = c->debug;
+    a.prefetch_tiles = c->prefetch_tiles;
     const SchedOptions o = effective_opts(c);
     // merge inside the attention launch when every CTA is resident at once
     // (the merging CTAs wait on the producing ones); else a merge launch

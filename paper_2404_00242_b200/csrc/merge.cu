@@ -17,7 +17,7 @@ namespace {
 using namespace dev;
 
 template <int DPL>
-__global__ void __launch_bounds__(128) merge_kernel(const AttnArgs a, int n_merge) {
+__global__ void __launch_bounds__(128, 8) merge_kernel(const AttnArgs a, int n_merge) {
     pdl_launch_dependents();
     const int wid = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;

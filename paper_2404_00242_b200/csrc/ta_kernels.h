@@ -54,6 +54,7 @@ struct AttnArgs {
     int out_bf16;
     long long* trace;         // optional clock64 trace (debug)
     int debug;                // debug experiment bits (0 in production)
+    int prefetch_tiles;       // first tiles of each CTA prefetched into L2 before the dependency wait
 };
 
 // tcgen05/TMEM path (bf16, D = 128).
