@@ -219,6 +219,7 @@ __global__ void __maxnreg__(160)
         }
     }
     pdl_wait();   // previous launch finished: queries, outputs, partial scratch are ours
+    if (threadIdx.x == 0) timeline_mark(a.timeline, 0, true);
     if (a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS] = gtimer();
         unsigned smid;
@@ -237,6 +238,7 @@ __global__ void __maxnreg__(160)
         // ===================== TMA producer =====================
         if (lane > 0) fill_empty(a, lane - 1, 31);
         if (lane == 0) {
+            const uint64_t pol_first = policy_evict_first();
             int gt = 0;
             for (int k = 0; k < n_items; ++k) {
                 const ItemDesc I = item_at(k);
@@ -254,8 +256,13 @@ __global__ void __maxnreg__(160)
                     for (int b = 0; b < td.nbox; ++b) {
                         const int g = td.box[b] >> 2, sz = td.box[b] & 3;
                         const int row = (int)(row0 + tmp->row[g]);
-                        tma_load_2d(kdst + g * 2048, &tm.k[sz], 0, row, BAR(FULLK + s));
-                        tma_load_2d(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s));
+                        if (a.evict_first) {
+                            tma_load_2d_hint(kdst + g * 2048, &tm.k[sz], 0, row, BAR(FULLK + s), pol_first);
+                            tma_load_2d_hint(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s), pol_first);
+                        } else {
+                            tma_load_2d(kdst + g * 2048, &tm.k[sz], 0, row, BAR(FULLK + s));
+                            tma_load_2d(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s));
+                        }
                     }
                     TA_TRACE(a, gt, 0);
                     mbar_wait(BAR(EMPTYV + s), ph ^ 1);
@@ -263,8 +270,13 @@ __global__ void __maxnreg__(160)
                     for (int b = 0; b < td.nbox; ++b) {
                         const int g = td.box[b] >> 2, sz = td.box[b] & 3;
                         const int row = (int)(row0 + tmp->row[g]);
-                        tma_load_2d(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + s));
-                        tma_load_2d(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + s));
+                        if (a.evict_first) {
+                            tma_load_2d_hint(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + s), pol_first);
+                            tma_load_2d_hint(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + s), pol_first);
+                        } else {
+                            tma_load_2d(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + s));
+                            tma_load_2d(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + s));
+                        }
                     }
                 }
             }
@@ -637,6 +649,33 @@ __global__ void __maxnreg__(160)
 
     tc_fence_before();
     __syncthreads();
+    if (a.grid_merge) {
+        // ---- split-K merge (tree_reduce, attention.hpp:209-233) in this launch:
+        // a grid-wide barrier (every CTA is resident: grid <= SM count), then
+        // every warp of every CTA merges records.  Release: CTA barrier + one
+        // gpu-scope fence before the arrival; acquire by the spinning thread.
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(a.merge_sync, 1);
+            while (true) {
+                int v;
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.merge_sync) : "memory");
+                if (v >= (int)gridDim.x) break;
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+        const int nw = (int)gridDim.x * (NTHREADS / 32);
+        const int n_task = a.n_merge * a.G;
+        for (int w = (int)blockIdx.x * (NTHREADS / 32) + warp; w < n_task; w += nw)
+            merge_record_row<4>(a, __ldg(a.merge_rec + w / a.G), w % a.G, lane);
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(a.merge_sync + 1, 1) == (int)gridDim.x - 1) {
+            a.merge_sync[0] = 0;   // the last CTA out resets both counters for the next launch
+            a.merge_sync[1] = 0;
+        }
+    }
+    if (threadIdx.x == 0) timeline_mark(a.timeline, 0, false);
     if (a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS + 1] = gtimer();
         int nt = 0;

@@ -66,9 +66,12 @@ struct ta_ctx {
     const int32_t* d_empty = nullptr;
     bool pdl = true;
     int prefetch_tiles = 3;
+    bool evict_first = true;
+    bool grid_merge = false;   // merge after a grid barrier inside the attention launch (measured slower)
     bool inline_merge = false;   // measured slower than the PDL-chained merge launch
     int64_t trace = 0;  // debug: device buffer for the MMA kernel's pipeline trace
     int debug = 0;      // debug experiment bits
+    int64_t timeline = 0;   // debug: per-launch start/end timestamps
     int num_sms = 148;
 
     // host copy of the schedule for ta_schedule_get
@@ -262,11 +265,17 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->opt.final_direct = v != 0;
         } else if (k == "pdl") {
             c->pdl = v != 0;
+        } else if (k == "evict_first") {
+            c->evict_first = v != 0;
+        } else if (k == "grid_merge") {
+            c->grid_merge = v != 0;
         } else if (k == "prefetch_tiles") {
             if (v < 0 || v > 32) fail(TA_ERR_INVALID_ARGUMENT, "prefetch_tiles must be in [0, 32]");
             c->prefetch_tiles = (int)v;
         } else if (k == "inline_merge") {
             c->inline_merge = v != 0;
+        } else if (k == "timeline_ptr") {
+            c->timeline = v;
         } else if (k == "trace_ptr") {
             c->trace = v;
         } else if (k == "debug") {
@@ -274,7 +283,10 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
         } else {
             fail(TA_ERR_INVALID_ARGUMENT, "unknown option " + k);
         }
-        c->prepared = false;
+        // launch-only knobs keep the prepared schedule
+        if (k != "trace_ptr" && k != "timeline_ptr" && k != "debug" && k != "pdl" && k != "prefetch_tiles" && k != "evict_first" &&
+            k != "grid_merge" && k != "inline_merge")
+            c->prepared = false;
     });
 }
 
@@ -585,16 +597,21 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.out_bf16 = c->shape.out_dtype == TA_BF16;
     a.trace = reinterpret_cast<long long*>(c->trace);
     a.debug = c->debug;
+    a.timeline = reinterpret_cast<unsigned long long*>(c->timeline);
     a.prefetch_tiles = c->prefetch_tiles;
+    a.evict_first = c->evict_first ? 1 : 0;
+
     const SchedOptions o = effective_opts(c);
     // merge inside the attention launch when every CTA is resident at once
     // (the merging CTAs wait on the producing ones); else a merge launch
     a.inline_merge = o.use_mma && c->inline_merge && a.n_ctas <= c->num_sms ? 1 : 0;
+    // grid barrier + merge by every CTA, when all CTAs are resident at once
+    a.grid_merge = !a.inline_merge && o.use_mma && c->grid_merge && a.n_ctas <= c->num_sms && a.n_merge > 0 ? 1 : 0;
     if (o.use_mma)
         cuda_check(launch_attn_mma(a, c->pdl, s), "attn_mma");
     else
         cuda_check(launch_attn_fma(a, o.fma_max_rows, c->pdl, s), "attn_fma");
-    if (!a.inline_merge) cuda_check(launch_merge(a, a.n_merge, c->pdl, s), "merge");
+    if (!a.inline_merge && !a.grid_merge) cuda_check(launch_merge(a, a.n_merge, c->pdl, s), "merge");
 }
 
 ta_status ta_attend(ta_ctx* c, int layer, const void* q, void* out, float* lse, void* stream) {
@@ -684,7 +701,7 @@ ta_status ta_schedule_get(ta_ctx* c, int bs, ta_schedule_view* o) {
 int ta_launches_per_attend(ta_ctx* c) {
     if (!c || !c->prepared) return 0;
     const SchedOptions o = effective_opts(c);
-    const bool inl = o.use_mma && c->inline_merge && (int)c->sched.cta_begin.size() - 1 <= c->num_sms;
+    const bool inl = o.use_mma && (c->inline_merge || c->grid_merge) && (int)c->sched.cta_begin.size() - 1 <= c->num_sms;
     return 1 + (c->sched.merge_leaf.empty() || inl ? 0 : 1);
 }
 

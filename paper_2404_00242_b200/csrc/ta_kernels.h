@@ -55,6 +55,9 @@ struct AttnArgs {
     long long* trace;         // optional clock64 trace (debug)
     int debug;                // debug experiment bits (0 in production)
     int prefetch_tiles;       // first tiles of each CTA prefetched into L2 before the dependency wait
+    int evict_first;          // stream KV with the L2 evict_first policy (read once per launch)
+    int grid_merge;           // merge after a grid-wide barrier in the attention launch (merge_sync[0..1])
+    unsigned long long* timeline;   // debug: [4] = attn first start, attn last end, merge first start, merge last end (ns)
 };
 
 // tcgen05/TMEM path (bf16, D = 128).

@@ -50,6 +50,20 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int 
 __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int c0, int c1) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(tmap), "r"(c0), "r"(c1) : "memory");
 }
+// L2 eviction policy for TMA (createpolicy): KV streamed once per launch is
+// evict_first, so it does not push out partials, metadata and queries
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const void* tmap, int c0, int c1, uint32_t bar,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(bar), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
@@ -124,6 +138,18 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 // state (queries, outputs, partials).
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// debug timeline: first start / last end of a launch (atomics on slots k, k+1)
+__device__ __forceinline__ void timeline_mark(unsigned long long* tl, int k, bool start) {
+    if (!tl) return;
+    if (start) atomicMin(tl + k, gtimer_ns());
+    else atomicMax(tl + k + 1, gtimer_ns());
+}
 
 // Store NV consecutive fp32 values (NV % 8 == 0) as the output dtype.
 template <int NV>
