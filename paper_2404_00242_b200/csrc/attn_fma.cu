@@ -76,12 +76,16 @@ struct FmaCfg {
     static_assert(TG >= 1 && TPW >= 1, "tile shape");
 };
 
+constexpr int FMAXI = 32, FMAXT = 48;   // staged items / tiles per CTA (the rest read from global)
+constexpr size_t FMETA_BYTES = FMAXI * 32 + 256 + FMAXT * (16 + 64);
+
 template <typename T, int D, int R>
 constexpr size_t fma_smem_bytes() {
     using C = FmaCfg<T, D>;
     return 2ull * 2 * C::TROWS * D * sizeof(T)            // K, V stages
            + (size_t)C::NW * 64 * 4                       // P buffers (64 per warp)
-           + (size_t)C::NW * R * (D + 2) * 4;             // warp combine
+           + (size_t)C::NW * R * (D + 2) * 4              // warp combine
+           + FMETA_BYTES;                                 // staged schedule
 }
 
 template <typename T, int D, int R>
@@ -103,42 +107,74 @@ __global__ void __launch_bounds__(256, 1) attn_fma_kernel(const AttnArgs a) {
     float* m_s = acc_s + NW * R * D;
     float* l_s = m_s + NW * R;
 
+    ItemDesc* s_item = reinterpret_cast<ItemDesc*>(l_s + NW * R);
+    int* s_ioff = reinterpret_cast<int*>(s_item + FMAXI);
+    TileDesc* s_td = reinterpret_cast<TileDesc*>(s_ioff + 64);
+    TileMeta* s_tm = reinterpret_cast<TileMeta*>(s_td + FMAXT);
+
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int it0 = a.cta_begin[blockIdx.x], it1 = a.cta_begin[blockIdx.x + 1];
+    const int n_items = it1 - it0;
     const int G = a.G;
+    // stage the CTA's schedule (host-written: read before the dependency wait)
+    const int ni_s = min(n_items, FMAXI);
+    for (int k = tid; k < ni_s; k += 256) s_item[k] = a.items[it0 + k];
+    __syncthreads();
+    if (tid == 0) {
+        int off = 0;
+        for (int k = 0; k < ni_s; ++k) {
+            s_ioff[k] = off;
+            off += s_item[k].tile_end - s_item[k].tile_begin;
+        }
+        s_ioff[ni_s] = off;
+    }
+    __syncthreads();
+    const int nt_s = min(s_ioff[ni_s], FMAXT);
+    for (int x = tid; x < nt_s; x += 256) {
+        int k = 0;
+        while (s_ioff[k + 1] <= x) ++k;
+        const int t = s_item[k].tile_begin + x - s_ioff[k];
+        s_td[x] = a.tiles[t];
+        s_tm[x] = a.tile_meta[t];
+    }
+    __syncthreads();
+    auto item_at = [&](int k) -> ItemDesc { return k < FMAXI ? s_item[k] : a.items[it0 + k]; };
+    auto td_at = [&](int lt, int t) -> TileDesc { return lt < nt_s ? s_td[lt] : a.tiles[t]; };
+    auto tm_at = [&](int lt, int t) -> const TileMeta* { return lt < nt_s ? &s_tm[lt] : &a.tile_meta[t]; };
     pdl_launch_dependents();
     pdl_wait();
     if (warp == NW - 1) fill_empty(a, lane);
-    if (it0 == it1) return;
+    if (n_items == 0) return;
 
-    // cp.async of one tile's K/V rows into stage st
-    auto issue = [&](int ii, int t, int st) {
-        const ItemDesc I = a.items[ii];
-        const TileDesc td = a.tiles[t];
+    // cp.async of one tile's K/V rows into stage st (tile t of item k, CTA tile lt)
+    auto issue = [&](int k, int t, int lt, int st) {
+        const ItemDesc I = item_at(k);
+        const TileDesc td = td_at(lt, t);
+        const TileMeta* tmp = tm_at(lt, t);
         const T* kb = reinterpret_cast<const T*>(a.k) + (size_t)I.head * a.head_stride;
         const T* vb = reinterpret_cast<const T*>(a.v) + (size_t)I.head * a.head_stride;
         const uint32_t ks = smem_u32(Ks + st * TROWS * D), vs = smem_u32(Vs + st * TROWS * D);
         for (int c = tid; c < td.ng * 16 * CPR; c += 256) {
             const int rr = c / CPR, ch = c % CPR;
-            const uint32_t info = a.grp_info[td.grp_begin + (rr >> 4)];
-            if ((rr & 15) >= (int)(info & 0xffu)) continue;
-            const size_t g = ((size_t)a.grp_row[td.grp_begin + (rr >> 4)] + (rr & 15)) * D;
+            if ((rr & 15) >= (int)(tmp->info[rr >> 4] & 0xffu)) continue;
+            const size_t g = ((size_t)tmp->row[rr >> 4] + (rr & 15)) * D;
             cp_async16(ks + (uint32_t)(rr * D * sizeof(T) + ch * 16), reinterpret_cast<const uint8_t*>(kb + g) + ch * 16);
             cp_async16(vs + (uint32_t)(rr * D * sizeof(T) + ch * 16), reinterpret_cast<const uint8_t*>(vb + g) + ch * 16);
         }
         cp_async_commit();
     };
     // (item, tile) cursor of the next tile to stage (runs ahead across items)
-    int nx_i = it0, nx_t = a.items[it0].tile_begin;
+    int nx_k = 0, nx_t = item_at(0).tile_begin, nx_lt = 0;
     auto advance = [&]() {
-        if (++nx_t >= a.items[nx_i].tile_end && ++nx_i < it1) nx_t = a.items[nx_i].tile_begin;
+        ++nx_lt;
+        if (++nx_t >= item_at(nx_k).tile_end && ++nx_k < n_items) nx_t = item_at(nx_k).tile_begin;
     };
-    issue(nx_i, nx_t, 0);
+    issue(nx_k, nx_t, nx_lt, 0);
     advance();
     int gt = 0;
 
-    for (int ii = it0; ii < it1; ++ii) {
-        const ItemDesc I = a.items[ii];
+    for (int ii = 0; ii < n_items; ++ii) {
+        const ItemDesc I = item_at(ii);
         const int nrows = I.n_slots * G;
         // queries of the item's rows in registers, pre-scaled by log2(e)/sqrt(D)
         float q[R][DPL];
@@ -167,17 +203,17 @@ __global__ void __launch_bounds__(256, 1) attn_fma_kernel(const AttnArgs a) {
 
         for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
             const int st = gt & 1;
-            if (nx_i < it1) {
-                issue(nx_i, nx_t, st ^ 1);
+            if (nx_k < n_items) {
+                issue(nx_k, nx_t, nx_lt, st ^ 1);
                 advance();
                 cp_async_wait<1>();
             } else {
                 cp_async_wait<0>();
             }
             __syncthreads();
-            const TileDesc td = a.tiles[t];
+            const TileDesc td = td_at(gt, t);
             const int grp = (warp * TPW) >> 4, c0 = (warp * TPW) & 15;
-            const uint32_t info = grp < td.ng ? a.grp_info[td.grp_begin + grp] : 0u;
+            const uint32_t info = grp < td.ng ? tm_at(gt, t)->info[grp] : 0u;
             const int cnt = max(0, min(TPW, (int)(info & 0xffu) - c0));    // valid tokens of this warp
             const int b = (int)((info >> 8) & 0xfffu), e = (int)(info >> 20);
             const T* Kst = Ks + (st * TROWS + warp * TPW) * D;
@@ -394,6 +430,7 @@ int fma_tile_groups(int D, int esize) {
 }
 
 cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, bool pdl, cudaStream_t s) {
+    if (max_rows <= 4) return a.kv_bf16 ? launch_fma_d<__nv_bfloat16, 4>(a, pdl, s) : launch_fma_d<float, 4>(a, pdl, s);
     if (max_rows <= 8) return a.kv_bf16 ? launch_fma_d<__nv_bfloat16, 8>(a, pdl, s) : launch_fma_d<float, 8>(a, pdl, s);
     return a.kv_bf16 ? launch_fma_d<__nv_bfloat16, 16>(a, pdl, s) : launch_fma_d<float, 16>(a, pdl, s);
 }

@@ -610,7 +610,7 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     if (o.use_mma)
         cuda_check(launch_attn_mma(a, c->pdl, s), "attn_mma");
     else
-        cuda_check(launch_attn_fma(a, o.fma_max_rows, c->pdl, s), "attn_fma");
+        cuda_check(launch_attn_fma(a, std::min(o.fma_max_rows, std::max(1, S.max_lane_rows)), c->pdl, s), "attn_fma");
     if (!a.inline_merge && !a.grid_merge) cuda_check(launch_merge(a, a.n_merge, c->pdl, s), "merge");
 }
 

@@ -566,6 +566,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
         }
     }
     S.n_lanes = (int32_t)lanes.size();
+    for (const Lane& ln : lanes) S.max_lane_rows = std::max<int32_t>(S.max_lane_rows, ln.n_slots * G);
     S.tile_meta.resize(S.tiles.size());
     for (std::size_t i = 0; i < S.tiles.size(); ++i) {
         TileMeta& tm = S.tile_meta[i];

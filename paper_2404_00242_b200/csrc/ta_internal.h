@@ -192,6 +192,7 @@ struct Schedule {
     std::vector<MergeRec> merge_rec;  // device copy: one 16-byte load per record
     std::vector<int32_t> empty;       // [n][2] (leaf, local head) pairs with no path tokens
     int32_t n_lanes = 0;
+    int32_t max_lane_rows = 0;        // max rows (slots x G) of any lane
     int32_t n_partials = 0;
     int32_t n_leaves = 0;
     int64_t kv_tokens_unique = 0;     // per kv head
