@@ -78,7 +78,7 @@ ta_status ta_ctx_create(int device, const ta_shape* shape, ta_ctx** out);
 ta_status ta_ctx_destroy(ta_ctx* ctx);
 /* tuning knobs: "use_mma", "fma_max_rows", "mma_max_rows", "tile_groups",
  * "tile_cost", "row_cost", "item_cost", "num_ctas", "final_direct", "pdl",
- * "inline_merge", "grid_merge", "prefetch_tiles", "evict_first"; debug:
+ * "prefetch_tiles"; debug:
  * "trace_ptr", "timeline_ptr", "debug" */
 ta_status ta_set_option(ta_ctx* ctx, const char* key, int64_t value);
 

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtreeattn_b200.so")
+LIB_PATH = os.environ.get("TREEATTN_B200_LIB") or os.path.join(_PKG, "libtreeattn_b200.so")   # env: A/B experiments
 
 TA_OK = 0
 TA_ERR_INVALID_ARGUMENT = 1

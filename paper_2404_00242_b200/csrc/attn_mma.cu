@@ -69,10 +69,8 @@ constexpr float kLazy = 8.0f;                            // rescale O only when 
 // Per-tile barriers are double-buffered by tile parity (S_FULL, S_FREE,
 // P_FULL, O_FULL): the softmax warps may run one tile ahead of the PV
 // issuer, and a waiter must never be two phases behind its barrier.
-// ITEM_DONE / ITEM_ACK: the softmax warps' partial stores of item k are
-// published (release) by helper lanes of warp 2 (in-kernel merge only).
 enum { FULLK = 0, FULLV = 3, EMPTYK = 6, EMPTYV = 9, S_FULL = 12, S_FREE = 14, P_FULL = 16, O_FULL = 18, Q_FULL = 20,
-       Q_FREE = 22, ITEM_DONE = 24, ITEM_ACK = 26, NBAR = 28 };
+       Q_FREE = 22, NBAR = 24 };
 constexpr int TMEM_SLOT = 240;                           // offset of the TMEM address in the barrier block
 static_assert(NBAR * 8 <= TMEM_SLOT, "barriers overlap the TMEM slot");
 
@@ -106,7 +104,7 @@ struct TmapSet {
     CUtensorMap v[4];
 };
 
-__global__ void __maxnreg__(160)
+__global__ void __launch_bounds__(NTHREADS, 1)
     attn_mma_kernel(const __grid_constant__ TmapSet tm, const AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -139,8 +137,6 @@ __global__ void __maxnreg__(160)
         for (int i = 0; i < 2; ++i) {
             mbar_init(BAR(Q_FULL + i), NSOFT);
             mbar_init(BAR(Q_FREE + i), 1);
-            mbar_init(BAR(ITEM_DONE + i), NSOFT);
-            mbar_init(BAR(ITEM_ACK + i), 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
@@ -238,7 +234,6 @@ __global__ void __maxnreg__(160)
         // ===================== TMA producer =====================
         if (lane > 0) fill_empty(a, lane - 1, 31);
         if (lane == 0) {
-            const uint64_t pol_first = policy_evict_first();
             int gt = 0;
             for (int k = 0; k < n_items; ++k) {
                 const ItemDesc I = item_at(k);
@@ -256,13 +251,8 @@ __global__ void __maxnreg__(160)
                     for (int b = 0; b < td.nbox; ++b) {
                         const int g = td.box[b] >> 2, sz = td.box[b] & 3;
                         const int row = (int)(row0 + tmp->row[g]);
-                        if (a.evict_first) {
-                            tma_load_2d_hint(kdst + g * 2048, &tm.k[sz], 0, row, BAR(FULLK + s), pol_first);
-                            tma_load_2d_hint(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s), pol_first);
-                        } else {
-                            tma_load_2d(kdst + g * 2048, &tm.k[sz], 0, row, BAR(FULLK + s));
-                            tma_load_2d(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s));
-                        }
+                        tma_load_2d(kdst + g * 2048, &tm.k[sz], 0, row, BAR(FULLK + s));
+                        tma_load_2d(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s));
                     }
                     TA_TRACE(a, gt, 0);
                     mbar_wait(BAR(EMPTYV + s), ph ^ 1);
@@ -270,13 +260,8 @@ __global__ void __maxnreg__(160)
                     for (int b = 0; b < td.nbox; ++b) {
                         const int g = td.box[b] >> 2, sz = td.box[b] & 3;
                         const int row = (int)(row0 + tmp->row[g]);
-                        if (a.evict_first) {
-                            tma_load_2d_hint(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + s), pol_first);
-                            tma_load_2d_hint(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + s), pol_first);
-                        } else {
-                            tma_load_2d(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + s));
-                            tma_load_2d(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + s));
-                        }
+                        tma_load_2d(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + s));
+                        tma_load_2d(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + s));
                     }
                 }
             }
@@ -333,24 +318,6 @@ __global__ void __maxnreg__(160)
                     mma_commit(BAR(S_FREE + sb));
                     mma_commit(BAR(O_FULL + sb));
                 }
-            }
-        } else if (a.inline_merge) {
-            // lanes 1..31: publish each item's partial records.  The softmax
-            // warps' stores are ordered before ITEM_DONE (mbarrier release);
-            // a gpu-scope fence here makes them visible before the arrival
-            // count of each record is bumped (merged by whichever CTA waits).
-            for (int k = 0; k < n_items; ++k) {
-                const ItemDesc I = item_at(k);
-                mbar_wait(BAR(ITEM_DONE + (k & 1)), (k >> 1) & 1);
-                if (I.pad & 1) {
-                    __threadfence();
-                    for (int jj = lane - 1; jj < I.n_slots; jj += 31) {
-                        const int cd = a.slot_out[I.out_begin + jj];
-                        if (cd >= 0) atomicAdd(a.merge_sync + 1 + a.part_merge[cd], 1);
-                    }
-                }
-                __syncwarp(0xfffffffeu);
-                if (lane == 1) mbar_arrive(BAR(ITEM_ACK + (k & 1)));
             }
         }
     } else {
@@ -606,75 +573,13 @@ __global__ void __maxnreg__(160)
             }
             TA_TRACE_EPI(a, k, 2);
             tc_fence_before();
-            if (a.inline_merge) {
-                if (k >= 2) mbar_wait(BAR(ITEM_ACK + (k & 1)), ((k - 2) >> 1) & 1);
-                mbar_arrive(BAR(ITEM_DONE + (k & 1)));
-            }
             if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt - 1, 7);
         }
 
-        if (a.inline_merge) {
-            // ---- merge (tree_reduce): every softmax warp of every CTA takes
-            // records off a global queue and merges each once all its partials
-            // have arrived.  All CTAs are resident, so the wait always ends.
-            const int total = (int)gridDim.x * 8;
-            const int n_task = a.n_merge * G;            // one task per (record, q head)
-            while (true) {
-                int tid_ = 0;
-                if (lane == 0) tid_ = atomicAdd(a.merge_sync, 1);
-                tid_ = __shfl_sync(0xffffffffu, tid_, 0);
-                if (tid_ >= n_task) {
-                    if (lane == 0 && tid_ == n_task + total - 1) a.merge_sync[0] = 0;   // last grab resets
-                    break;
-                }
-                const int rid = tid_ / G, g = tid_ % G;
-                const int4 rec = __ldg(a.merge_rec + rid);
-                if (lane == 0) {
-                    while (true) {
-                        int v;
-                        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.merge_sync + 1 + rid) : "memory");
-                        if (v >= rec.w) break;
-                        __nanosleep(a.debug >> 8);
-                    }
-                }
-                __syncwarp();
-                __threadfence();   // every lane: acquire side of the partials it reads
-                merge_record_row<4>(a, rec, g, lane);
-                // the record's last task to finish resets its arrival count
-                __syncwarp();
-                if (lane == 0 && atomicAdd(a.merge_sync + 1 + rid, 1) == rec.w + G - 1) a.merge_sync[1 + rid] = 0;
-            }
-        }
     }
 
     tc_fence_before();
     __syncthreads();
-    if (a.grid_merge) {
-        // ---- split-K merge (tree_reduce, attention.hpp:209-233) in this launch:
-        // a grid-wide barrier (every CTA is resident: grid <= SM count), then
-        // every warp of every CTA merges records.  Release: CTA barrier + one
-        // gpu-scope fence before the arrival; acquire by the spinning thread.
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(a.merge_sync, 1);
-            while (true) {
-                int v;
-                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.merge_sync) : "memory");
-                if (v >= (int)gridDim.x) break;
-                __nanosleep(64);
-            }
-        }
-        __syncthreads();
-        const int nw = (int)gridDim.x * (NTHREADS / 32);
-        const int n_task = a.n_merge * a.G;
-        for (int w = (int)blockIdx.x * (NTHREADS / 32) + warp; w < n_task; w += nw)
-            merge_record_row<4>(a, __ldg(a.merge_rec + w / a.G), w % a.G, lane);
-        __syncthreads();
-        if (threadIdx.x == 0 && atomicAdd(a.merge_sync + 1, 1) == (int)gridDim.x - 1) {
-            a.merge_sync[0] = 0;   // the last CTA out resets both counters for the next launch
-            a.merge_sync[1] = 0;
-        }
-    }
     if (threadIdx.x == 0) timeline_mark(a.timeline, 0, false);
     if (a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS + 1] = gtimer();

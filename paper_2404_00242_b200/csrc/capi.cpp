@@ -61,14 +61,9 @@ struct ta_ctx {
     const int32_t* d_slot_out = nullptr;
     const int4* d_merge_rec = nullptr;
     const int32_t* d_part_merge = nullptr;
-    int* merge_sync = nullptr;      // in-kernel merge queue + arrival counters (self-resetting)
-    size_t merge_sync_cap = 0;      // bytes
     const int32_t* d_empty = nullptr;
     bool pdl = true;
     int prefetch_tiles = 3;
-    bool evict_first = true;
-    bool grid_merge = false;   // merge after a grid barrier inside the attention launch (measured slower)
-    bool inline_merge = false;   // measured slower than the PDL-chained merge launch
     int64_t trace = 0;  // debug: device buffer for the MMA kernel's pipeline trace
     int debug = 0;      // debug experiment bits
     int64_t timeline = 0;   // debug: per-launch start/end timestamps
@@ -97,7 +92,6 @@ struct ta_ctx {
             cudaFree(meta_dev);
             cudaFreeHost(meta_host);
             cudaFree(part);
-            cudaFree(merge_sync);
             cudaFree(stage_dev);
             cudaFreeHost(stage_host);
             cudaFree(io_dev);
@@ -265,15 +259,9 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->opt.final_direct = v != 0;
         } else if (k == "pdl") {
             c->pdl = v != 0;
-        } else if (k == "evict_first") {
-            c->evict_first = v != 0;
-        } else if (k == "grid_merge") {
-            c->grid_merge = v != 0;
         } else if (k == "prefetch_tiles") {
             if (v < 0 || v > 32) fail(TA_ERR_INVALID_ARGUMENT, "prefetch_tiles must be in [0, 32]");
             c->prefetch_tiles = (int)v;
-        } else if (k == "inline_merge") {
-            c->inline_merge = v != 0;
         } else if (k == "timeline_ptr") {
             c->timeline = v;
         } else if (k == "trace_ptr") {
@@ -284,8 +272,7 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             fail(TA_ERR_INVALID_ARGUMENT, "unknown option " + k);
         }
         // launch-only knobs keep the prepared schedule
-        if (k != "trace_ptr" && k != "timeline_ptr" && k != "debug" && k != "pdl" && k != "prefetch_tiles" && k != "evict_first" &&
-            k != "grid_merge" && k != "inline_merge")
+        if (k != "trace_ptr" && k != "timeline_ptr" && k != "debug" && k != "pdl" && k != "prefetch_tiles")
             c->prepared = false;
     });
 }
@@ -540,15 +527,6 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             c->part = (float*)p;
             c->part_cap = cap / sizeof(float);
         }
-        const size_t ms = (S.merge_rec.size() + 1) * sizeof(int);
-        if (ms > c->merge_sync_cap) {
-            // earlier launches may still use the old counters
-            cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-            void* p = c->merge_sync;
-            grow_dev(&p, &c->merge_sync_cap, ms);
-            c->merge_sync = (int*)p;
-            cuda_check(cudaMemset(c->merge_sync, 0, c->merge_sync_cap), "cudaMemset(merge_sync)");
-        }
         c->prepared = true;
         c->prepared_version = c->tree.version;
         c->prepared_bs = bs;
@@ -584,7 +562,6 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.slot_out = c->d_slot_out;
     a.merge_rec = c->d_merge_rec;
     a.part_merge = c->d_part_merge;
-    a.merge_sync = c->merge_sync;
     a.n_merge = (int)S.merge_rec.size();
     a.empty = c->d_empty;
     a.n_empty = (int)(S.empty.size() / 2);
@@ -599,19 +576,15 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.debug = c->debug;
     a.timeline = reinterpret_cast<unsigned long long*>(c->timeline);
     a.prefetch_tiles = c->prefetch_tiles;
-    a.evict_first = c->evict_first ? 1 : 0;
 
     const SchedOptions o = effective_opts(c);
     // merge inside the attention launch when every CTA is resident at once
     // (the merging CTAs wait on the producing ones); else a merge launch
-    a.inline_merge = o.use_mma && c->inline_merge && a.n_ctas <= c->num_sms ? 1 : 0;
-    // grid barrier + merge by every CTA, when all CTAs are resident at once
-    a.grid_merge = !a.inline_merge && o.use_mma && c->grid_merge && a.n_ctas <= c->num_sms && a.n_merge > 0 ? 1 : 0;
     if (o.use_mma)
         cuda_check(launch_attn_mma(a, c->pdl, s), "attn_mma");
     else
         cuda_check(launch_attn_fma(a, std::min(o.fma_max_rows, std::max(1, S.max_lane_rows)), c->pdl, s), "attn_fma");
-    if (!a.inline_merge && !a.grid_merge) cuda_check(launch_merge(a, a.n_merge, c->pdl, s), "merge");
+    cuda_check(launch_merge(a, a.n_merge, c->pdl, s), "merge");
 }
 
 ta_status ta_attend(ta_ctx* c, int layer, const void* q, void* out, float* lse, void* stream) {
@@ -700,9 +673,7 @@ ta_status ta_schedule_get(ta_ctx* c, int bs, ta_schedule_view* o) {
 
 int ta_launches_per_attend(ta_ctx* c) {
     if (!c || !c->prepared) return 0;
-    const SchedOptions o = effective_opts(c);
-    const bool inl = o.use_mma && (c->inline_merge || c->grid_merge) && (int)c->sched.cta_begin.size() - 1 <= c->num_sms;
-    return 1 + (c->sched.merge_leaf.empty() || inl ? 0 : 1);
+    return 1 + (c->sched.merge_leaf.empty() ? 0 : 1);
 }
 
 }  // extern "C"

@@ -40,9 +40,7 @@ struct AttnArgs {
     const int32_t* slot_out;
     const int4* merge_rec;    // [n_merge] {leaf, local kv head, first partial id, count}
     const int32_t* part_merge;// partial id -> merge record
-    int* merge_sync;          // [0] record queue, [1 + mi] arrivals of record mi (self-resetting)
-    int n_merge;
-    int inline_merge;         // merge inside the attention launch (all CTAs co-resident)
+    int n_merge;              // merge records
     const int32_t* empty;     // [n_empty][2] (leaf, head)
     int n_empty;
     int n_ctas;
@@ -55,8 +53,6 @@ struct AttnArgs {
     long long* trace;         // optional clock64 trace (debug)
     int debug;                // debug experiment bits (0 in production)
     int prefetch_tiles;       // first tiles of each CTA prefetched into L2 before the dependency wait
-    int evict_first;          // stream KV with the L2 evict_first policy (read once per launch)
-    int grid_merge;           // merge after a grid-wide barrier in the attention launch (merge_sync[0..1])
     unsigned long long* timeline;   // debug: [4] = attn first start, attn last end, merge first start, merge last end (ns)
 };
 
