@@ -69,8 +69,8 @@ constexpr float kLazy = 8.0f;                            // rescale O only when 
 // Per-tile barriers are double-buffered by tile parity (S_FULL, S_FREE,
 // P_FULL, O_FULL): the softmax warps may run one tile ahead of the PV
 // issuer, and a waiter must never be two phases behind its barrier.
-enum { FULLK = 0, FULLV = 3, EMPTYK = 6, EMPTYV = 9, S_FULL = 12, S_FREE = 14, P_FULL = 16, O_FULL = 18, Q_FULL = 20,
-       Q_FREE = 22, NBAR = 24 };
+enum { FULLK = 0, FULLV = NSTAGE, EMPTYK = 2 * NSTAGE, EMPTYV = 3 * NSTAGE, S_FULL = 4 * NSTAGE, S_FREE = S_FULL + 2,
+       P_FULL = S_FULL + 4, O_FULL = S_FULL + 6, Q_FULL = S_FULL + 8, Q_FREE = S_FULL + 10, NBAR = S_FULL + 12 };
 constexpr int TMEM_SLOT = 240;                           // offset of the TMEM address in the barrier block
 static_assert(NBAR * 8 <= TMEM_SLOT, "barriers overlap the TMEM slot");
 
