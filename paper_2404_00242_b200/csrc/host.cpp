@@ -448,7 +448,7 @@ struct Lane {
 
 void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G, int n_heads,
                     const SchedOptions& opt, Schedule& S) {
-    S = Schedule{};
+    S.clear();   // keeps the vectors' capacity: no reallocation (and page faults) per step
     S.n_leaves = (int32_t)t.leaves.size();
     const int P = pool.page_size;
     const int nc = plan.n_chunks();
@@ -541,22 +541,33 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                     if (bb >= ee) continue;
                     const auto& h = pool.handle(plan.cseg_node[s]);
                     const int64_t off = plan.cseg_offset[s], len = plan.cseg_len[s];
-                    for (int64_t k2 = 0; k2 < len; ++k2) {
+                    // runs of consecutive pool rows (within a page) are added in bulk
+                    for (int64_t k2 = 0; k2 < len;) {
                         const int64_t tok = off + k2;
-                        const int32_t row = (int32_t)(h.pages[tok / P] * P + tok % P);
-                        if (g_open >= 0) {
-                            const uint32_t info = S.grp_info[g_open];
-                            const int cnt = (int)(info & 0xffu);
-                            if (cnt < 16 && S.grp_row[g_open] + cnt == row && (int)((info >> 8) & 0xfffu) == bb &&
-                                (int)(info >> 20) == ee) {
-                                S.grp_info[g_open] = grp_pack(cnt + 1, bb, ee);
-                                continue;
+                        int32_t row = (int32_t)(h.pages[tok / P] * P + tok % P);
+                        int run = (int)std::min<int64_t>(len - k2, P - tok % P);
+                        k2 += run;
+                        while (run > 0) {
+                            if (g_open >= 0) {
+                                const uint32_t info = S.grp_info[g_open];
+                                const int cnt = (int)(info & 0xffu);
+                                if (cnt < 16 && S.grp_row[g_open] + cnt == row && (int)((info >> 8) & 0xfffu) == bb &&
+                                    (int)(info >> 20) == ee) {
+                                    const int take = std::min(run, 16 - cnt);
+                                    S.grp_info[g_open] = grp_pack(cnt + take, bb, ee);
+                                    row += take;
+                                    run -= take;
+                                    continue;
+                                }
                             }
+                            if ((int32_t)S.grp_row.size() - tile_g0 == TG) close_tile(false);
+                            g_open = (int32_t)S.grp_row.size();
+                            const int take = std::min(run, 16);
+                            S.grp_row.push_back(row);
+                            S.grp_info.push_back(grp_pack(take, bb, ee));
+                            row += take;
+                            run -= take;
                         }
-                        if ((int32_t)S.grp_row.size() - tile_g0 == TG) close_tile(false);
-                        g_open = (int32_t)S.grp_row.size();
-                        S.grp_row.push_back(row);
-                        S.grp_info.push_back(grp_pack(1, bb, ee));
                     }
                 }
             }
@@ -631,16 +642,18 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     // ---- 4. outputs: touched slots, direct vs partial, merge lists
     const int L = S.n_leaves;
     std::vector<int32_t> cover((size_t)L * n_heads, 0);
-    std::vector<uint8_t> touched;
+    std::vector<int32_t> touched;   // slot-range coverage as a difference array: O(groups + slots)
     for (ItemDesc& it : S.items) {
-        touched.assign(it.n_slots, 0);
+        touched.assign(it.n_slots + 1, 0);
         for (int i = it.tile_begin; i < it.tile_end; ++i) {
             const TileDesc& td = S.tiles[i];
             for (int g = 0; g < td.ng; ++g) {
                 const uint32_t info = S.grp_info[td.grp_begin + g];
-                for (int j = (int)((info >> 8) & 0xfffu); j < (int)(info >> 20); ++j) touched[j] = 1;
+                touched[(info >> 8) & 0xfffu]++;
+                touched[info >> 20]--;
             }
         }
+        for (int j = 1; j <= it.n_slots; ++j) touched[j] += touched[j - 1];
         it.out_begin = (int32_t)S.slot_out.size();
         for (int j = 0; j < it.n_slots; ++j) {
             if (touched[j]) {
@@ -655,7 +668,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     // [merge_begin[mi], merge_begin[mi+1]) in item order), so the merge reads
     // them without an id list
     std::vector<int32_t> rec((size_t)L * n_heads, -1);  // leaf-head -> merge record
-    std::vector<std::vector<int32_t*>> rec_codes;
+    std::vector<int32_t> rec_n;                          // partials per record (counting sort)
     for (const ItemDesc& it : S.items) {
         for (int j = 0; j < it.n_slots; ++j) {
             int32_t& code = S.slot_out[it.out_begin + j];
@@ -667,24 +680,35 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                 continue;
             }
             if (rec[key] < 0) {
-                rec[key] = (int32_t)rec_codes.size();
-                rec_codes.emplace_back();
+                rec[key] = (int32_t)rec_n.size();
+                rec_n.push_back(0);
                 S.merge_leaf.push_back(leaf);
                 S.merge_head.push_back(it.head);
             }
-            rec_codes[rec[key]].push_back(&code);
+            code = rec[key];   // temporarily: the record
+            rec_n[rec[key]]++;
         }
     }
-    S.merge_begin.assign(1, 0);
-    for (std::size_t mi = 0; mi < rec_codes.size(); ++mi) {
-        for (int32_t* c : rec_codes[mi]) {
-            *c = S.n_partials++;
-            S.part_merge.push_back((int32_t)mi);
-            S.merge_parts.push_back(*c);
+    const int nrec = (int)rec_n.size();
+    S.merge_begin.resize(nrec + 1);
+    S.merge_begin[0] = 0;
+    for (int mi = 0; mi < nrec; ++mi) S.merge_begin[mi + 1] = S.merge_begin[mi] + rec_n[mi];
+    S.n_partials = S.merge_begin[nrec];
+    S.part_merge.resize(S.n_partials);
+    S.merge_parts.resize(S.n_partials);
+    std::vector<int32_t> fill(S.merge_begin.begin(), S.merge_begin.end() - 1);
+    for (const ItemDesc& it : S.items)   // item order within each record
+        for (int j = 0; j < it.n_slots; ++j) {
+            int32_t& code = S.slot_out[it.out_begin + j];
+            if (code < 0) continue;
+            const int mi = code;
+            code = fill[mi]++;
+            S.part_merge[code] = mi;
+            S.merge_parts[code] = code;
         }
-        S.merge_begin.push_back(S.n_partials);
-        S.merge_rec.push_back({S.merge_leaf[mi], S.merge_head[mi], S.merge_begin[mi], S.n_partials - S.merge_begin[mi]});
-    }
+    S.merge_rec.resize(nrec);
+    for (int mi = 0; mi < nrec; ++mi)
+        S.merge_rec[mi] = {S.merge_leaf[mi], S.merge_head[mi], S.merge_begin[mi], rec_n[mi]};
     for (ItemDesc& it : S.items)
         for (int j = 0; j < it.n_slots; ++j)
             if (S.slot_out[it.out_begin + j] >= 0) it.pad |= 1;   // holds partials: takes part in merges

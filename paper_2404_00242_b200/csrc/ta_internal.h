@@ -199,6 +199,14 @@ struct Schedule {
     int64_t kv_rows_loaded = 0;       // box rows loaded, all local heads
     int64_t masked_q_tokens = 0;      // sum over leaves of path tokens (flops / (4 d h_q))
     int64_t n_stripes = 0;
+
+    void clear() {
+        tiles.clear(); tile_meta.clear(); grp_row.clear(); grp_info.clear(); items.clear(); cta_begin.clear();
+        slot_leaf.clear(); slot_out.clear(); part_merge.clear(); merge_leaf.clear(); merge_head.clear();
+        merge_begin.clear(); merge_parts.clear(); merge_rec.clear(); empty.clear();
+        n_lanes = n_partials = n_leaves = max_lane_rows = 0;
+        kv_tokens_unique = kv_rows_loaded = masked_q_tokens = n_stripes = 0;
+    }
 };
 
 struct SchedOptions {
