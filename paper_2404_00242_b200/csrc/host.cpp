@@ -589,8 +589,10 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     }
 
     // ---- 3. CTA runs over the (head, lane, tile) sequence.  Cost of a tile:
-    // its box rows (bytes) + a fixed per-tile cost + a softmax cost growing
-    // with the lane's rows; every item a CTA starts costs item_cost more.
+    // its box rows (KV bytes) + a fixed per-tile cost + a softmax cost growing
+    // with its attended (row, token) pairs; every item a CTA starts costs
+    // item_cost more.  (A max(streaming, softmax) model and an L2 discount for
+    // the re-read row blocks of wide stripes measured worse.)
     const int n_tiles = (int)S.tiles.size();
     std::vector<int32_t> tile_lane(n_tiles);
     for (int li = 0; li < (int)lanes.size(); ++li)
@@ -598,8 +600,13 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     std::vector<int64_t> tcost(n_tiles);
     int64_t per_head = (int64_t)opt.item_cost * (int64_t)lanes.size();
     for (int i = 0; i < n_tiles; ++i) {
-        const int rows = lanes[tile_lane[i]].n_slots * G;
-        tcost[i] = 16LL * S.tiles[i].ng + opt.tile_cost + (int64_t)opt.row_cost * rows / 128;
+        // softmax work: attended (row, token) pairs, in units of a dense 128 x 128 tile
+        int64_t pairs = 0;
+        for (int g = 0; g < S.tiles[i].ng; ++g) {
+            const uint32_t info = S.grp_info[S.tiles[i].grp_begin + g];
+            pairs += (int64_t)(info & 0xffu) * (int64_t)((info >> 20) - ((info >> 8) & 0xfffu)) * G;
+        }
+        tcost[i] = 16LL * S.tiles[i].ng + opt.tile_cost + (int64_t)opt.row_cost * pairs / (128 * 128);
         per_head += tcost[i];
         S.kv_rows_loaded += 16LL * S.tiles[i].ng * n_heads;
     }

@@ -85,3 +85,13 @@ for c in range(n_cta):
 for rows in sorted(groups):
     v = np.array(groups[rows]).mean(0)
     print(f"  {rows:4d} {len(groups[rows]):5d} " + " ".join(f"{x:8.0f}" for x in v))
+
+# CTA duration by (items, rows of each item, tiles): what the cost model must capture
+print("\nCTA duration by shape: n_items rows... tiles -> n, mean dur us")
+shape = {}
+for c in range(n_cta):
+    its = list(range(S["cta_begin"][c], S["cta_begin"][c + 1]))
+    key = (len(its), tuple(int(S["items"][i][4]) * ctx.group for i in its), int(t[c, 3]))
+    shape.setdefault(key, []).append(dur[c])
+for k in sorted(shape, key=lambda k: -np.mean(shape[k]))[:14]:
+    print(f"  {k}: n={len(shape[k])} {np.mean(shape[k]):.2f}")
