@@ -89,7 +89,10 @@ class TreeAttention:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().ta_ctx_destroy(self._h)
+            try:
+                lib().ta_ctx_destroy(self._h)
+            except Exception:   # interpreter teardown: modules already gone
+                pass
             self._h = None
 
     def __del__(self):

@@ -4,8 +4,10 @@
 // tiles of one lane for one kv head, see ta_internal.h).  Rows of an item
 // are (query slot, q head in the GQA group) pairs, <= 128 of them, one per
 // TMEM lane.  Per tile (<= 8 groups of 16 pool rows = <= 128 tokens):
-//   TMA (warp 0)    K/V boxes -> SMEM ring (128B swizzle), 3 stages, K and V
-//                   on separate barriers; runs ahead across items
+//   TMA (warp 0)    K/V boxes -> SMEM ring (128B swizzle), 2 stages, K and V
+//                   on separate barriers; runs ahead across items.  Two stages
+//                   per SM already keep HBM saturated; a deeper ring only adds
+//                   queueing latency (paid at every CTA's start and end)
 //   QK  (warp 1)    S = Q K^T  (M=128, N=16*groups, K=128), Q from TMEM
 //                   -> S buffer (t & 1) in TMEM
 //   PV  (warp 2)    O += P V   (M=128, N=128, K=16*groups), P from TMEM
@@ -37,7 +39,7 @@ using namespace dev;
 
 constexpr int BM = 128;                                  // rows per item (TMEM lanes)
 constexpr int DH = 128;                                  // head dim
-constexpr int NSTAGE = 3;                                // KV ring depth
+constexpr int NSTAGE = 2;                                // KV ring depth
 constexpr int HALF = BM * 128;                           // one 64-column half of a [128][128] bf16 tile
 constexpr int TILE = 2 * HALF;                           // 32 KB
 constexpr int STAGE = 2 * TILE;                          // K + V

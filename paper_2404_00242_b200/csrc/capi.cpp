@@ -63,7 +63,7 @@ struct ta_ctx {
     const int32_t* d_part_merge = nullptr;
     const int32_t* d_empty = nullptr;
     bool pdl = true;
-    int prefetch_tiles = 3;
+    int prefetch_tiles = 2;
     int64_t trace = 0;  // debug: device buffer for the MMA kernel's pipeline trace
     int debug = 0;      // debug experiment bits
     int64_t timeline = 0;   // debug: per-launch start/end timestamps
