@@ -77,18 +77,20 @@ constexpr int TMEM_SLOT = 240;                           // offset of the TMEM a
 static_assert(NBAR * 8 <= TMEM_SLOT, "barriers overlap the TMEM slot");
 
 // Optional pipeline trace (debug; AttnArgs::trace != nullptr): per CTA 256
-// int64 slots: [0] start / [1] end (%globaltimer ns), [2] SM id, [3] tiles,
-// then per tile t < 31 (clock64, 8 slots): [8+8t] K loads issued, [+1] S
+// int64 slots: [0] start / [1] end (%globaltimer ns), [2] SM id, [3] tiles, [4] / [5] clock64 at start / end,
+// then per tile t < 27 (clock64, 8 slots): [8+8t] K loads issued, [+1] S
 // seen by softmax, [+2] S loaded + masked, [+3] row max exchanged, [+4]
 // O_FULL(t-1) seen, [+5] O rescaled, [+6] P published, [+7] item epilogue
 // done (last tile of an item only).
-constexpr int TRACE_SLOTS = 256, TRACE_TILES = 31;
+constexpr int TRACE_SLOTS = 256, TRACE_TILES = 27;   // tiles: slots 8..223
 __device__ __forceinline__ long long gtimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// epilogue phases: slots 240.. for the CTA's first item, 248.. for its last
+// epilogue phases ([0] O_FULL seen, [1] fenced, [4] l exchanged, [3] stores begin, [2]
+// stores done): slots 240.. for the CTA's first item, 248.. for its last; slot
+// 224 + w: softmax warp w's last epilogue end; 232 + c: O columns c loaded
 #define TA_TRACE_EPI(a, item, k)                                                                   \
     do {                                                                                           \
         if ((a).trace && threadIdx.x == TRACE_TID) {                                               \
@@ -118,6 +120,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     float* redl = reinterpret_cast<float*>(smem + SMEM_REDL);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0 && a.timeline) {   // debug: CTA entry (first / last over the grid)
+        timeline_mark(a.timeline, 4, true);
+        timeline_mark(a.timeline, 4, false);
+    }
     const int it0 = a.cta_begin[blockIdx.x], it1 = a.cta_begin[blockIdx.x + 1];
     const int n_items = it1 - it0;
     ItemDesc* s_item = reinterpret_cast<ItemDesc*>(smem + SMEM_ITEM);
@@ -190,6 +196,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncthreads();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0 && a.timeline) {   // debug: schedule staged
+        timeline_mark(a.timeline, 6, true);
+        timeline_mark(a.timeline, 6, false);
+    }
     pdl_launch_dependents();
     // warm L2 with the first tiles' KV and the first item's query rows while
     // the previous launch drains (prefetches carry no ordering obligations)
@@ -220,6 +230,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (threadIdx.x == 0) timeline_mark(a.timeline, 0, true);
     if (a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS] = gtimer();
+        a.trace[blockIdx.x * TRACE_SLOTS + 4] = clock64();
         unsigned smid;
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
         a.trace[blockIdx.x * TRACE_SLOTS + 2] = smid;
@@ -514,6 +525,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             redl[h * BM + r] = l;
             named_bar(1 + q4, 64);
             l += redl[(h ^ 1) * BM + r];
+            TA_TRACE_EPI(a, k, 4);
             const float inv = l > 0.f ? 1.f / l : 0.f;
             const float lse2 = m + log2f(l);
             if (code != kSlotUnused && h == 0) {
@@ -540,6 +552,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int col = h * 64 + c * 16;
                     TA_TMEM_LD16(tmem + lane_addr + TMEM_O + col, o);
                     tmem_wait_ld();
+                    if (a.trace && threadIdx.x == TRACE_TID) a.trace[blockIdx.x * TRACE_SLOTS + 232 + c] = clock64();
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
                         sts128(epi + (uint32_t)(lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)),
@@ -576,6 +589,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             TA_TRACE_EPI(a, k, 2);
             tc_fence_before();
             if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt - 1, 7);
+            if (a.trace && lane == 0) a.trace[blockIdx.x * TRACE_SLOTS + 224 + warp - SOFT0] = clock64();
         }
 
     }
@@ -585,6 +599,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (threadIdx.x == 0) timeline_mark(a.timeline, 0, false);
     if (a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS + 1] = gtimer();
+        a.trace[blockIdx.x * TRACE_SLOTS + 5] = clock64();
         int nt = 0;
         for (int k = 0; k < n_items; ++k) nt += item_at(k).tile_end - item_at(k).tile_begin;
         a.trace[blockIdx.x * TRACE_SLOTS + 3] = nt;

@@ -26,8 +26,9 @@ __global__ void __launch_bounds__(128, 8) merge_kernel(const AttnArgs a, int n_m
     // the record is host-written schedule metadata: read it before the wait
     const int4 rec = live ? __ldg(a.merge_rec + mi) : make_int4(0, 0, 0, 0);   // leaf, head, first partial, count
     pdl_wait();   // the attention launch's partials are complete
-    if (!live) return;
-    merge_record_row<DPL>(a, rec, g, lane);
+    if (threadIdx.x == 0) timeline_mark(a.timeline, 2, true);
+    if (live) merge_record_row<DPL>(a, rec, g, lane);
+    if (threadIdx.x == 0) timeline_mark(a.timeline, 2, false);
 }
 
 }  // namespace

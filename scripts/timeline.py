@@ -38,7 +38,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 tls = []
 for layer in range(n):
-    tl = torch.tensor([2**63 - 1, 0, 2**63 - 1, 0], dtype=torch.int64, device="cuda")
+    tl = torch.tensor([2**63 - 1, 0, 2**63 - 1, 0, 2**63 - 1, 0, 2**63 - 1, 0], dtype=torch.int64, device="cuda")
     tls.append(tl)
 ctx.prepare(128)
 torch.cuda.synchronize()
@@ -47,8 +47,10 @@ for layer in range(n):
     ctx.attend(layer, q[layer], out[layer])
 torch.cuda.synchronize()
 t0 = int(tls[0][0])
-print(f"{name}: per layer (us rel. to layer 0 attention start): attn start/end, merge start/end, attn+merge")
+print(f"{name}: per layer (us rel. to layer 0 attention start): attn start/end, merge start/end, "
+      "CTA entry first/last, staged first/last")
 for layer in range(n):
     a = [int(x) for x in tls[layer].cpu()]
     ms = "-" if a[2] > 2**62 else f"{(a[2] - t0) / 1e3:8.2f} {(a[3] - t0) / 1e3:8.2f}"
-    print(f"  {layer}: {(a[0] - t0) / 1e3:8.2f} {(a[1] - t0) / 1e3:8.2f}   {ms}   dur {(a[1] - a[0]) / 1e3:.2f}")
+    ex = "" if a[4] > 2**62 else " ".join(f"{(x - t0) / 1e3:8.2f}" for x in a[4:8])
+    print(f"  {layer}: {(a[0] - t0) / 1e3:8.2f} {(a[1] - t0) / 1e3:8.2f}   {ms}   {ex}   dur {(a[1] - a[0]) / 1e3:.2f}")
