@@ -381,9 +381,13 @@ def main():
         on = oh.view(torch.int16).numpy() if dt == torch.bfloat16 else oh.numpy()
 
         def step_host():
+            # one decode step through the host-buffer entry: the n_layers
+            # calls pipeline copy-in / attention / copy-out; the step ends
+            # when every layer's output is back in host memory
             ctx.prepare(128, stream)
             for layer in range(L_layers):
-                ctx.attend_host(layer, qn[layer], on[layer], stream=stream)
+                ctx.attend_host_async(layer, qn[layer], on[layer], stream=stream)
+            ctx.attend_host_wait()
 
         for _ in range(2):
             step_host()
@@ -407,7 +411,8 @@ def main():
         e2e = {"value": ems * 1000.0, "unit": "us/decode step",
                "h2d_bytes_per_step": int(q.numel() * q.element_size()),
                "d2h_bytes_per_step": int(out.numel() * out.element_size()),
-               "path": "ta_prepare + ta_attend_host per layer (host q in, host out back, synchronised)"}
+               "path": "ta_prepare + ta_attend_host_async per layer (pinned host q in, host out back; copy-in, "
+                        "attention and copy-out of consecutive layers overlap) + ta_attend_host_wait per step"}
 
     if rank != 0:
         if world > 1:

@@ -150,6 +150,16 @@ ta_status ta_attend(ta_ctx* ctx, int layer, const void* q, void* out, float* lse
  * D2H out, synchronised on `stream` before returning. */
 ta_status ta_attend_host(ta_ctx* ctx, int layer, const void* q_host, void* out_host,
                          void* stream);
+/* Pipelined host-buffer variant: enqueues H2D q (context copy-in stream),
+ * attend (on `stream`), D2H out (context copy-out stream) and returns.
+ * Consecutive calls overlap the copy-in of one call, the attention of the
+ * previous one and the copy-out of the one before (three device slots).  Host
+ * buffers should be pinned for the copies to be asynchronous; out_host is
+ * complete after ta_attend_host_wait.  Reference analogue: run_iteration's
+ * host-side inputs and AttentionOutput (attention.hpp:293-334), batched. */
+ta_status ta_attend_host_async(ta_ctx* ctx, int layer, const void* q_host, void* out_host,
+                               void* stream);
+ta_status ta_attend_host_wait(ta_ctx* ctx);
 
 typedef struct ta_io_stats {
     int64_t n_chunks;          /* flatten chunks (sibling groups fused) */

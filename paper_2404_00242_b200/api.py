@@ -215,6 +215,16 @@ class TreeAttention:
               "attend_host")
         return out_host
 
+    def attend_host_async(self, layer: int, q_host, out_host, stream=None):
+        """Pipelined host-buffer attend: returns once queued; out_host is complete
+        after attend_host_wait().  Use pinned host buffers for overlap."""
+        check(lib().ta_attend_host_async(self._h, int(layer), _ptr(q_host), _ptr(out_host), _stream(stream)),
+              "attend_host_async")
+        return out_host
+
+    def attend_host_wait(self):
+        check(lib().ta_attend_host_wait(self._h), "attend_host_wait")
+
     def io_stats(self) -> IoStats:
         s = capi.IoStats()
         check(lib().ta_io_stats_get(self._h, C.byref(s)), "io_stats")

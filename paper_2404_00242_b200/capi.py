@@ -26,7 +26,7 @@ EXPORTED = [
     "ta_last_error", "ta_abi_version", "ta_ctx_create", "ta_ctx_destroy", "ta_set_option",
     "ta_tree_new", "ta_tree_restore", "ta_tree_branch", "ta_tree_prune", "ta_tree_append",
     "ta_tree_leaves", "ta_tree_get_info", "ta_tree_snapshot", "ta_pool_stats", "ta_pool_token_ref",
-    "ta_kv_write", "ta_plan_flatten", "ta_plan_json", "ta_prepare", "ta_attend", "ta_attend_host",
+    "ta_kv_write", "ta_plan_flatten", "ta_plan_json", "ta_prepare", "ta_attend", "ta_attend_host", "ta_attend_host_async", "ta_attend_host_wait",
     "ta_io_stats_get", "ta_launches_per_attend", "ta_schedule_get",
 ]
 
@@ -139,6 +139,8 @@ def lib():
         "ta_prepare": (C.c_int, [vp, C.c_int, vp]),
         "ta_attend": (C.c_int, [vp, C.c_int, vp, vp, vp, vp]),
         "ta_attend_host": (C.c_int, [vp, C.c_int, vp, vp, vp]),
+        "ta_attend_host_async": (C.c_int, [vp, C.c_int, vp, vp, vp]),
+        "ta_attend_host_wait": (C.c_int, [vp]),
         "ta_io_stats_get": (C.c_int, [vp, C.POINTER(IoStats)]),
         "ta_launches_per_attend": (C.c_int, [vp]),
         "ta_schedule_get": (C.c_int, [vp, C.c_int, C.POINTER(ScheduleView)]),

@@ -83,6 +83,19 @@ struct ta_ctx {
     size_t stage_host_cap = 0;
     void* io_dev = nullptr;
     size_t io_cap = 0;
+    // pipelined host-buffer attend (ta_attend_host_async): a ring of device
+    // q / out slots; H2D and D2H on their own streams so that consecutive
+    // calls overlap copy-in, attention and copy-out
+    static constexpr int kIoSlots = 3;
+    struct IoSlot {
+        void* dev = nullptr;
+        size_t cap = 0;
+        cudaEvent_t h2d = nullptr, kern = nullptr, d2h = nullptr;
+        bool used = false;
+    };
+    IoSlot io_slot[kIoSlots];
+    int io_next = 0;
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
 
     ~ta_ctx() {
         if (device >= 0) {
@@ -95,6 +108,14 @@ struct ta_ctx {
             cudaFree(stage_dev);
             cudaFreeHost(stage_host);
             cudaFree(io_dev);
+            for (IoSlot& sl : io_slot) {
+                cudaFree(sl.dev);
+                if (sl.h2d) cudaEventDestroy(sl.h2d);
+                if (sl.kern) cudaEventDestroy(sl.kern);
+                if (sl.d2h) cudaEventDestroy(sl.d2h);
+            }
+            if (h2d_stream) cudaStreamDestroy(h2d_stream);
+            if (d2h_stream) cudaStreamDestroy(d2h_stream);
             if (meta_done) cudaEventDestroy(meta_done);
         }
     }
@@ -609,6 +630,57 @@ ta_status ta_attend_host(ta_ctx* c, int layer, const void* q_host, void* out_hos
         attend_impl(c, layer, dq, dout, nullptr, s);
         cuda_check(cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, s), "D2H out");
         cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    });
+}
+
+ta_status ta_attend_host_async(ta_ctx* c, int layer, const void* q_host, void* out_host, void* stream) {
+    return guard([&] {
+        need_device(c);
+        cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+        cudaStream_t s = (cudaStream_t)stream;
+        if (!c->h2d_stream) {
+            cuda_check(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            cuda_check(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            for (auto& sl : c->io_slot) {
+                cuda_check(cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming), "cudaEventCreate");
+                cuda_check(cudaEventCreateWithFlags(&sl.kern, cudaEventDisableTiming), "cudaEventCreate");
+                cuda_check(cudaEventCreateWithFlags(&sl.d2h, cudaEventDisableTiming), "cudaEventCreate");
+            }
+        }
+        const size_t L = c->tree.leaves.size();
+        const size_t qb = L * c->hq_loc * c->shape.d_head * c->esize;
+        const size_t ob = L * c->hq_loc * c->shape.d_head * c->out_esize;
+        const size_t need = align_up(qb, 256) + ob;
+        auto& sl = c->io_slot[c->io_next];
+        c->io_next = (c->io_next + 1) % ta_ctx::kIoSlots;
+        if (need > sl.cap) {
+            if (sl.used) cuda_check(cudaEventSynchronize(sl.d2h), "cudaEventSynchronize");
+            cudaFree(sl.dev);
+            sl.dev = nullptr;
+            sl.cap = 0;
+            cuda_check(cudaMalloc(&sl.dev, need), "cudaMalloc(io slot)");
+            sl.cap = need;
+        }
+        char* dq = (char*)sl.dev;
+        char* dout = dq + align_up(qb, 256);
+        // the slot's previous use (its copy-out, hence its attention) is complete
+        if (sl.used) cuda_check(cudaStreamWaitEvent(c->h2d_stream, sl.d2h, 0), "cudaStreamWaitEvent");
+        cuda_check(cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, c->h2d_stream), "H2D q");
+        cuda_check(cudaEventRecord(sl.h2d, c->h2d_stream), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(s, sl.h2d, 0), "cudaStreamWaitEvent");
+        attend_impl(c, layer, dq, dout, nullptr, s);
+        cuda_check(cudaEventRecord(sl.kern, s), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(c->d2h_stream, sl.kern, 0), "cudaStreamWaitEvent");
+        cuda_check(cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, c->d2h_stream), "D2H out");
+        cuda_check(cudaEventRecord(sl.d2h, c->d2h_stream), "cudaEventRecord");
+        sl.used = true;
+    });
+}
+
+ta_status ta_attend_host_wait(ta_ctx* c) {
+    return guard([&] {
+        need_device(c);
+        if (c->d2h_stream) cuda_check(cudaStreamSynchronize(c->d2h_stream), "cudaStreamSynchronize");
     });
 }
 

@@ -203,7 +203,8 @@ def test_config_b_few_shot_full_size():
 
 
 def test_multilayer_and_host_entry():
-    """Per-layer pools are independent; ta_attend_host == ta_attend."""
+    """Per-layer pools are independent; ta_attend_host and the pipelined
+    ta_attend_host_async == ta_attend."""
     import torch
     from paper_2404_00242_b200 import TreeAttention
     t = core.Tree(500)
@@ -224,6 +225,18 @@ def test_multilayer_and_host_entry():
         oh = np.zeros((len(leaves), 8, 128), np.float32)
         ctx.attend_host(l, qh, oh)
         assert np.array_equal(oh.reshape(len(leaves), -1), out)
+    # pipelined host entry: all layers queued back to back (pinned buffers,
+    # more layers than device slots), identical results
+    import torch
+    qs = [q_tensor(ctx, c, leaves) for c in cs]
+    ref = [ctx.attend(l, qs[l]).float().cpu().numpy().reshape(len(leaves), -1) for l in range(3)]
+    qp = [qs[l].cpu().view(torch.int16).pin_memory() for l in range(3)]
+    op = [torch.zeros((len(leaves), 8, 128), dtype=torch.float32).pin_memory() for _ in range(7)]
+    for i in range(7):
+        ctx.attend_host_async(i % 3, qp[i % 3].numpy(), op[i].numpy())
+    ctx.attend_host_wait()
+    for i in range(7):
+        assert np.array_equal(op[i].numpy().reshape(len(leaves), -1), ref[i % 3])
 
 
 # ------------------------------------------------------- schedule variations
