@@ -38,7 +38,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 tls = []
 for layer in range(n):
-    tl = torch.tensor([2**63 - 1, 0, 2**63 - 1, 0, 2**63 - 1, 0, 2**63 - 1, 0], dtype=torch.int64, device="cuda")
+    tl = torch.tensor([2**63 - 1, 0] * 5, dtype=torch.int64, device="cuda")
     tls.append(tl)
 ctx.prepare(128)
 torch.cuda.synchronize()
@@ -53,4 +53,6 @@ for layer in range(n):
     a = [int(x) for x in tls[layer].cpu()]
     ms = "-" if a[2] > 2**62 else f"{(a[2] - t0) / 1e3:8.2f} {(a[3] - t0) / 1e3:8.2f}"
     ex = "" if a[4] > 2**62 else " ".join(f"{(x - t0) / 1e3:8.2f}" for x in a[4:8])
+    if a[8] < 2**62:
+        ex += "   merge entry " + " ".join(f"{(x - t0) / 1e3:8.2f}" for x in a[8:10])
     print(f"  {layer}: {(a[0] - t0) / 1e3:8.2f} {(a[1] - t0) / 1e3:8.2f}   {ms}   {ex}   dur {(a[1] - a[0]) / 1e3:.2f}")

@@ -142,3 +142,4 @@ for c in range(n_cta):
 r_ = np.array(rows_)
 for nm, col in zip(["start->S(0)", "P(last)->O_full", "O_full->l_xchg", "l_xchg->loop", "loop->ld0", "ld0->ld1", "ld2->ld3", "ld3->stored", "stored->all warps", "warps->end", "end"], r_.T):
     print(f"  {nm:16s} min {np.nanmin(col):6.2f} median {np.nanmedian(col):6.2f} max {np.nanmax(col):6.2f} us")
+
