@@ -50,8 +50,12 @@ constexpr int SMEM_REDL = SMEM_RED + 2 * 2 * BM * 4;     // [2 half][128] fp32 r
 // the CTA's schedule, staged once before the dependency wait: items, their
 // tile offsets in the CTA's tile sequence, tile descriptors and metadata
 constexpr int MAXI = 32, MAXT = 112;
-constexpr int SMEM_EPI = SMEM_REDL + 2 * BM * 4;        // [8 warps][32 rows][64 B] epilogue staging
-constexpr int SMEM_ITEM = SMEM_EPI + 8 * 32 * 64;        // ItemDesc[MAXI]
+// epilogue staging: one row of O / l (this thread's 64 columns) per thread,
+// 256 B + 16 B pad (conflict-free 16-byte stores), written to global by one
+// bulk async copy per row
+constexpr int EPI_ROW = 272;
+constexpr int SMEM_EPI = SMEM_REDL + 2 * BM * 4;        // [8 warps][32 rows][EPI_ROW]
+constexpr int SMEM_ITEM = SMEM_EPI + 8 * 32 * EPI_ROW;   // ItemDesc[MAXI]
 constexpr int SMEM_IOFF = SMEM_ITEM + MAXI * 32;         // int[MAXI + 1]
 constexpr int SMEM_TD = SMEM_IOFF + 256;                 // TileDesc[MAXT]
 constexpr int SMEM_TM = SMEM_TD + MAXT * 16;             // TileMeta[MAXT]
@@ -536,54 +540,48 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             if (warp_live) {
-                // O / l -> final output or partial record, 16 columns at a time:
-                // row-wise into this warp's SMEM staging (chunks swizzled by
-                // (row >> 1) & 3: conflict-free both ways), then every store
-                // instruction writes 8 rows x 64 contiguous bytes.  Compact
-                // loops: this code runs once per item, I-cache cold.
-                const uint32_t epi = sbase + SMEM_EPI + (uint32_t)(warp - SOFT0) * 2048;
-                int dcode[4];
-#pragma unroll
-                for (int s4 = 0; s4 < 4; ++s4) dcode[s4] = __shfl_sync(0xffffffffu, code, 8 * s4 + (lane >> 2));
+                // O / l -> this thread's staging row (its TMEM lane = output row,
+                // its 64 columns), then one bulk async copy of the row to the
+                // final output or the partial record: the stores drain in the
+                // background instead of stalling the softmax warps behind the
+                // saturated read stream.  Compact loops: this code runs once per
+                // item, I-cache cold.
+                const uint32_t srow = sbase + SMEM_EPI + (uint32_t)(((warp - SOFT0) * 32 + lane) * EPI_ROW);
+                const bool st_bf16 = code < 0 && a.out_bf16;
+                // the row's previous bulk copy (an earlier item) has read the staging
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 TA_TRACE_EPI(a, k, 3);
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     uint32_t o[16];
-                    const int col = h * 64 + c * 16;
-                    TA_TMEM_LD16(tmem + lane_addr + TMEM_O + col, o);
+                    TA_TMEM_LD16(tmem + lane_addr + TMEM_O + h * 64 + c * 16, o);
                     tmem_wait_ld();
                     if (a.trace && threadIdx.x == TRACE_TID) a.trace[blockIdx.x * TRACE_SLOTS + 232 + c] = clock64();
+                    float f[16];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        sts128(epi + (uint32_t)(lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)),
-                               __float_as_uint(__uint_as_float(o[4 * q]) * inv),
-                               __float_as_uint(__uint_as_float(o[4 * q + 1]) * inv),
-                               __float_as_uint(__uint_as_float(o[4 * q + 2]) * inv),
-                               __float_as_uint(__uint_as_float(o[4 * q + 3]) * inv));
-                    __syncwarp();
+                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(o[i]) * inv;
+                    if (st_bf16) {
+                        sts128(srow + (uint32_t)(c * 32), pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]),
+                               pack_bf16(f[6], f[7]));
+                        sts128(srow + (uint32_t)(c * 32 + 16), pack_bf16(f[8], f[9]), pack_bf16(f[10], f[11]),
+                               pack_bf16(f[12], f[13]), pack_bf16(f[14], f[15]));
+                    } else {
 #pragma unroll
-                    for (int s4 = 0; s4 < 4; ++s4) {
-                        const int rl = 8 * s4 + (lane >> 2), ch = lane & 3;   // staged row, 16-byte chunk
-                        const int cd = dcode[s4];
-                        float4 v;
-                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                                     : "r"(epi + (uint32_t)(rl * 64 + ((ch ^ ((rl >> 1) & 3)) << 4)))
-                                     : "memory");
-                        if (cd == kSlotUnused || (a.debug & 1)) continue;
-                        const int gq = (q4 * 32 + rl) % G, c0 = col + 4 * ch;
-                        if (cd < 0) {
-                            const size_t o_ = ((size_t)(-1 - cd) * a.hq_loc + I.head * G + gq) * DH + c0;
-                            if (a.out_bf16)
-                                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + o_) =
-                                    make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
-                            else
-                                *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + o_) = v;
-                        } else {
-                            *reinterpret_cast<float4*>(a.part_o + ((size_t)cd * G + gq) * DH + c0) = v;
-                        }
+                        for (int q = 0; q < 4; ++q)
+                            sts128(srow + (uint32_t)(c * 64 + 16 * q), __float_as_uint(f[4 * q]), __float_as_uint(f[4 * q + 1]),
+                                   __float_as_uint(f[4 * q + 2]), __float_as_uint(f[4 * q + 3]));
                     }
-                    __syncwarp();
+                }
+                if (code != kSlotUnused && !(a.debug & 1)) {
+                    void* dst = code >= 0 ? static_cast<void*>(a.part_o + ((size_t)code * G + g_in) * DH + 64 * h)
+                                          : static_cast<void*>(reinterpret_cast<char*>(a.out) +
+                                                               (((size_t)(-1 - code) * a.hq_loc + I.head * G + g_in) * DH + 64 * h) *
+                                                                   (a.out_bf16 ? 2 : 4));
+                    fence_proxy_async();   // the staging writes -> visible to the bulk copy
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(srow),
+                                 "r"(st_bf16 ? 128u : 256u)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
             }
             TA_TRACE_EPI(a, k, 2);
@@ -594,6 +592,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     }
 
+    // the epilogues' bulk copies are complete (writes performed) before exit
+    if (warp >= SOFT0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) timeline_mark(a.timeline, 0, false);

@@ -599,6 +599,8 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.prefetch_tiles = c->prefetch_tiles;
 
     const SchedOptions o = effective_opts(c);
+    if (o.use_mma && (((uintptr_t)out | (uintptr_t)q) & 15))
+        fail(TA_ERR_INVALID_ARGUMENT, "attend: q and out must be 16-byte aligned");
     // merge inside the attention launch when every CTA is resident at once
     // (the merging CTAs wait on the producing ones); else a merge launch
     if (o.use_mma)
