@@ -53,6 +53,8 @@ t0 = t[:, 0].min()
 start = (t[:, 0] - t0) / 1e3
 end = (t[:, 1] - t0) / 1e3
 dur = end - start
+os.makedirs("gpurun_out", exist_ok=True)
+np.save(f"gpurun_out/dur_{name}.npy", np.stack([start, end]))
 print(f"{name}: CTAs {n_cta}, kernel span {end.max():.2f} us, start spread {start.max():.2f} us, "
       f"dur min/mean/max {dur.min():.2f}/{dur.mean():.2f}/{dur.max():.2f} us")
 for c in list(np.argsort(-dur)[:3]) + list(np.argsort(dur)[:2]):
