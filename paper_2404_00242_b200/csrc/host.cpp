@@ -598,7 +598,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     for (int li = 0; li < (int)lanes.size(); ++li)
         for (int i = lanes[li].tile_begin; i < lanes[li].tile_end; ++i) tile_lane[i] = li;
     std::vector<int64_t> tcost(n_tiles);
-    int64_t per_head = (int64_t)opt.item_cost * (int64_t)lanes.size();
+    int64_t tile_sum = 0;   // per head
     for (int i = 0; i < n_tiles; ++i) {
         // softmax work: attended (row, token) pairs, in units of a dense 128 x 128 tile
         int64_t pairs = 0;
@@ -607,14 +607,17 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
             pairs += (int64_t)(info & 0xffu) * (int64_t)((info >> 20) - ((info >> 8) & 0xfffu)) * G;
         }
         tcost[i] = 16LL * S.tiles[i].ng + opt.tile_cost + (int64_t)opt.row_cost * pairs / (128 * 128);
-        per_head += tcost[i];
+        tile_sum += tcost[i];
         S.kv_rows_loaded += 16LL * S.tiles[i].ng * n_heads;
     }
     const int n_cta = std::max(1, opt.num_ctas);
-    // each CTA boundary opens one more item than the (head, lane) count
-    const int64_t total = per_head * n_heads + (int64_t)opt.item_cost * (n_cta - 1);
-    S.cta_begin.assign(1, 0);
-    {
+    // returns the most items any CTA got
+    auto partition = [&](int item_cost) -> int {
+        S.items.clear();
+        S.cta_begin.assign(1, 0);
+        const int64_t per_head = (int64_t)item_cost * (int64_t)lanes.size() + tile_sum;
+        // each CTA boundary opens one more item than the (head, lane) count
+        const int64_t total = per_head * n_heads + (int64_t)item_cost * (n_cta - 1);
         int cta = 0;
         int64_t acc = 0;
         ItemDesc* open = nullptr;
@@ -637,14 +640,23 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                     it.n_slots = lanes[li].n_slots;
                     S.items.push_back(it);
                     open = &S.items.back();
-                    acc += opt.item_cost;
+                    acc += item_cost;
                 }
                 open->tile_end = i + 1;
                 acc += tcost[i];
             }
         }
         while ((int)S.cta_begin.size() < n_cta + 1) S.cta_begin.push_back((int32_t)S.items.size());
-    }
+        int most = 0;
+        for (int c = 0; c < n_cta; ++c) most = std::max(most, S.cta_begin[c + 1] - S.cta_begin[c]);
+        return most;
+    };
+    // Item switches cost 3.6-4.6 us each (per-CTA fit of traced durations,
+    // profiles/r1_summary.md): where CTAs would run many short items (token
+    // trees, many small branches) they are charged more, which measured
+    // faster there (spec t256 -9 %); schedules of few long items keep the
+    // base cost (few-shot is faster with it).
+    if (partition(opt.item_cost) > opt.many_items && opt.item_cost_many > opt.item_cost) partition(opt.item_cost_many);
 
     // ---- 4. outputs: touched slots, direct vs partial, merge lists
     const int L = S.n_leaves;

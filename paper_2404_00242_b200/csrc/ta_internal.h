@@ -217,6 +217,8 @@ struct SchedOptions {
     int row_cost = 15;         // softmax cost of a dense tile (128 x 128 attended pairs), in box rows
                                // (swept: 15 beats 60 by 3 % on few-shot, 14 % on 70B, ties on reasoning)
     int item_cost = 300;       // cost of starting an item (Q load, epilogue), in box rows
+    int item_cost_many = 450;  // ... when the base cost leaves some CTA more than many_items items
+    int many_items = 4;
     bool use_mma = true;       // bf16 d128 only
     int fma_max_rows = 8;      // rows per lane of the FMA kernel (8 or 16)
     bool final_direct = true;  // single-item leaf-heads written directly
