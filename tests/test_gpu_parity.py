@@ -246,6 +246,7 @@ def test_mma_cta_counts_and_fma_bf16():
     rng = core.Rng(31)
     t = core.random_tree(rng, max_leaves=60, max_node_tokens=300)
     for opts in ({"num_ctas": 1}, {"num_ctas": 7}, {"num_ctas": 600}, {"tile_groups": 3},
+                 {"many_items": 1, "item_cost_many": 2000},
                  {"use_mma": 0, "fma_max_rows": 8}, {"use_mma": 0, "fma_max_rows": 16}):
         _gqa_case(t, 128, 32, 8, 13, options=opts)
 
