@@ -276,6 +276,8 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
         } else if (k == "item_cost_many") {
             if (v < 0) fail(TA_ERR_INVALID_ARGUMENT, "item_cost_many must be >= 0");
             c->opt.item_cost_many = (int)v;
+        } else if (k == "minmax") {
+            c->opt.minmax = v != 0;
         } else if (k == "many_items") {
             if (v < 1) fail(TA_ERR_INVALID_ARGUMENT, "many_items must be >= 1");
             c->opt.many_items = (int)v;

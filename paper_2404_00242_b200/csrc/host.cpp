@@ -651,6 +651,106 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
         for (int c = 0; c < n_cta; ++c) most = std::max(most, S.cta_begin[c + 1] - S.cta_begin[c]);
         return most;
     };
+    // Min-max variant: the smallest per-CTA budget B for which a greedy cut of
+    // the sequence into runs of cost <= B needs at most n_cta runs (binary
+    // search on B; each greedy pass finds a run's end by galloping search on
+    // prefix sums of tile costs and lane-segment starts).  The equal-split
+    // cut above rounds every boundary to a tile edge and can leave the
+    // heaviest CTA up to a tile plus an item over the mean.
+    auto partition_minmax = [&](int item_cost) -> int {
+        const int64_t N = (int64_t)n_heads * n_tiles;
+        if (N == 0) {
+            S.items.clear();
+            S.cta_begin.assign(n_cta + 1, 0);
+            return 0;
+        }
+        // prefix sums over the sequence (kept across calls: no page faults per step):
+        // P[x] = cost of positions [0, x), NB[x] = lane-segment starts at positions 1..x
+        static thread_local std::vector<int64_t> P;
+        static thread_local std::vector<int32_t> NB;
+        P.resize(N + 1);
+        NB.resize(N + 1);
+        P[0] = 0;
+        int64_t maxt = 0;
+        {
+            int64_t x = 0;
+            int32_t nb = 0;
+            for (int h = 0; h < n_heads; ++h)
+                for (int i = 0; i < n_tiles; ++i, ++x) {
+                    P[x + 1] = P[x] + tcost[i];
+                    maxt = std::max(maxt, tcost[i]);
+                    if (x > 0 && (i == 0 || tile_lane[i] != tile_lane[i - 1])) ++nb;
+                    NB[x] = nb;
+                }
+        }
+        auto cost = [&](int64_t a, int64_t b) { return P[b] - P[a] + (int64_t)item_cost * (1 + NB[b - 1] - NB[a]); };
+        auto runs = [&](int64_t cap, std::vector<int64_t>* cuts) {
+            int64_t a = 0;
+            int n = 0;
+            while (a < N) {
+                // the largest b with cost(a, b) <= cap (at least a + 1): gallop, then bisect
+                int64_t step = 1, ok = a + 1;
+                while (ok + step <= N && cost(a, ok + step) <= cap) {
+                    ok += step;
+                    step *= 2;
+                }
+                int64_t lo = ok, hi = std::min(N, ok + step - 1);
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi + 1) / 2;
+                    if (cost(a, mid) <= cap) lo = mid; else hi = mid - 1;
+                }
+                if (cuts) cuts->push_back(lo);
+                a = lo;
+                ++n;
+            }
+            return n;
+        };
+        const int64_t total = cost(0, N);
+        int64_t lo = std::max<int64_t>(maxt + item_cost, (total + n_cta - 1) / n_cta), hi = lo;
+        while (runs(hi, nullptr) > n_cta) hi += hi - lo + maxt + item_cost;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (runs(mid, nullptr) <= n_cta) hi = mid; else lo = mid + 1;
+        }
+        std::vector<int64_t> cuts;
+        runs(lo, &cuts);
+        S.items.clear();
+        S.cta_begin.assign(1, 0);
+        int64_t a = 0;
+        int h = 0, i = 0;   // position a as (head, tile)
+        for (const int64_t b : cuts) {
+            ItemDesc* open = nullptr;
+            for (int64_t x = a; x < b; ++x, ++i) {
+                if (i == n_tiles) {
+                    i = 0;
+                    ++h;
+                }
+                const int li = tile_lane[i];
+                if (!open || open->head != h || open->lane != li) {
+                    ItemDesc it{};
+                    it.head = h;
+                    it.lane = li;
+                    it.tile_begin = i;
+                    it.tile_end = i;
+                    it.slot_begin = lanes[li].slot_begin;
+                    it.n_slots = lanes[li].n_slots;
+                    S.items.push_back(it);
+                    open = &S.items.back();
+                }
+                open->tile_end = i + 1;
+            }
+            S.cta_begin.push_back((int32_t)S.items.size());
+            a = b;
+        }
+        while ((int)S.cta_begin.size() < n_cta + 1) S.cta_begin.push_back((int32_t)S.items.size());
+        int most = 0;
+        for (int c = 0; c < n_cta; ++c) most = std::max(most, S.cta_begin[c + 1] - S.cta_begin[c]);
+        return most;
+    };
+    if (opt.minmax) {
+        if (partition_minmax(opt.item_cost) > opt.many_items && opt.item_cost_many > opt.item_cost)
+            partition_minmax(opt.item_cost_many);
+    } else
     // Item switches cost 3.6-4.6 us each (per-CTA fit of traced durations,
     // profiles/r1_summary.md): where CTAs would run many short items (token
     // trees, many small branches) they are charged more, which measured

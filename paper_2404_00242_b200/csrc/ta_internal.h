@@ -219,6 +219,8 @@ struct SchedOptions {
     int item_cost = 300;       // cost of starting an item (Q load, epilogue), in box rows
     int item_cost_many = 450;  // ... when the base cost leaves some CTA more than many_items items
     int many_items = 4;
+    int minmax = 1;            // CTA runs: 1 min-max budget (binary search; measured better on
+                               // every config), 0 equal split points
     bool use_mma = true;       // bf16 d128 only
     int fma_max_rows = 8;      // rows per lane of the FMA kernel (8 or 16)
     bool final_direct = true;  // single-item leaf-heads written directly
