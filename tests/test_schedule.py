@@ -214,14 +214,15 @@ def test_coverage_zero_token_and_holders():
 
 
 def test_coverage_item_cost_repartition():
-    """The re-partition with the higher item cost (CTAs with many items) keeps
-    the coverage contract and the oracle result."""
+    """The re-partition with the higher item cost (CTAs with many items) and
+    both CTA partitions keep the coverage contract."""
     rng = core.Rng(404)
     for trial in range(6):
         ctx = _ctx(G=4, dtype="bf16", n_kv=2)
         ctx.set_option("many_items", 1)          # always re-partition
         ctx.set_option("item_cost_many", (450, 5000)[trial % 2])
         ctx.set_option("num_ctas", (13, 148)[trial % 2])
+        ctx.set_option("minmax", trial % 3 != 2)   # min-max budget / equal split points
         t = core.random_tree(rng, max_leaves=50, max_node_tokens=200)
         ctx.restore(*t.snapshot())
         check_coverage(ctx, t, 128)
