@@ -701,13 +701,15 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                 }
                 if (cuts) cuts->push_back(lo);
                 a = lo;
-                ++n;
+                if (++n > n_cta && !cuts) return n;   // infeasible budget: stop counting
             }
             return n;
         };
         const int64_t total = cost(0, N);
-        int64_t lo = std::max<int64_t>(maxt + item_cost, (total + n_cta - 1) / n_cta), hi = lo;
-        while (runs(hi, nullptr) > n_cta) hi += hi - lo + maxt + item_cost;
+        // greedy with budget >= mean + largest piece never needs more than n_cta runs
+        int64_t lo = std::max<int64_t>(maxt + item_cost, (total + n_cta - 1) / n_cta);
+        int64_t hi = (total + n_cta - 1) / n_cta + maxt + item_cost;
+        while (runs(hi, nullptr) > n_cta) hi += maxt + item_cost;   // (defensive)
         while (lo < hi) {
             const int64_t mid = (lo + hi) / 2;
             if (runs(mid, nullptr) <= n_cta) hi = mid; else lo = mid + 1;
