@@ -15,5 +15,5 @@ for c in few_shot reasoning spec_t64 demo; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"attn_|merge" -s 40 -c 2 -f -o gpurun_out/final/prof_$c $B > gpurun_out/final/ncu_$c.log 2>&1
   timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"attn_|merge" -s 40 -c 16 --csv --log-file gpurun_out/final/launches_$c.csv $B > /dev/null 2>&1
 done
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final/launches_default.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"attn_mma|attn_fma|merge_kernel" -c 256 --csv --log-file gpurun_out/final/launches_default.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 ls gpurun_out/final
