@@ -180,6 +180,31 @@ def test_speculative_token_tree_holders_bf16():
     _gqa_case(core.Tree.from_snapshot(snap), 128, 32, 8, 5)
 
 
+def test_misaligned_buffers_rejected():
+    """The tcgen05 path moves q and out rows in 16-byte units (and the
+    epilogue by bulk copies): misaligned buffers fail loudly, as the
+    reference's invalid_argument (ValueError)."""
+    import torch
+    from paper_2404_00242_b200 import TreeAttention
+    t = core.Tree(300)
+    t.branch(t.root, [20, 40])
+    c = make_content(t, 128, 8, 8, 1, bf16=True)
+    ctx = TreeAttention(n_layers=1, n_q_heads=8, n_kv_heads=8, d_head=128, kv_dtype="bf16", max_pages=64)
+    ctx.restore(*t.snapshot())
+    load_into(ctx, c)
+    ctx.prepare(128)
+    leaves = ctx.leaves()
+    q = q_tensor(ctx, c, leaves)
+    flat = torch.empty(q.numel() + 8, dtype=torch.bfloat16, device="cuda")
+    qm = flat[4:4 + q.numel()].view(q.shape)   # 8-byte offset
+    qm.copy_(q)
+    with pytest.raises(ValueError):
+        ctx.attend(0, qm)
+    out = ctx.attend(0, q)   # aligned: fine
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+
+
 def test_bf16_out_dtype():
     t = core.Tree(300)
     t.branch(t.root, [20, 40])
