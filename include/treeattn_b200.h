@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define TA_ABI_VERSION 1
+#define TA_ABI_VERSION 2
 
 typedef int ta_status;
 enum {
@@ -77,9 +77,9 @@ int ta_abi_version(void);
 ta_status ta_ctx_create(int device, const ta_shape* shape, ta_ctx** out);
 ta_status ta_ctx_destroy(ta_ctx* ctx);
 /* tuning knobs: "use_mma", "fma_max_rows", "mma_max_rows", "tile_groups",
- * "tile_cost", "row_cost", "item_cost", "num_ctas", "final_direct", "pdl",
- * "prefetch_tiles"; debug:
- * "trace_ptr", "timeline_ptr", "debug" */
+ * "tile_cost", "row_cost", "item_cost", "item_cost_many", "many_items",
+ * "minmax", "num_ctas", "final_direct", "fused_merge", "pdl",
+ * "prefetch_tiles"; debug: "trace_ptr", "timeline_ptr" */
 ta_status ta_set_option(ta_ctx* ctx, const char* key, int64_t value);
 
 /* ---- DecodingTree (tree mutations drive the page pool like KvLifecycle) -- */
@@ -213,6 +213,9 @@ typedef struct ta_schedule_view {
     const int32_t* empty;       /* [n_empty][2] (leaf, local kv head) */
     int32_t n_lanes;
     int32_t use_mma;
+    int32_t fused_merge;        /* 1: slot_out codes >= 2^30 mark the item that merges record
+                                   code - 2^30 inside the attention launch (merge_parts then
+                                   lists the other items' partials only) */
 } ta_schedule_view;
 ta_status ta_schedule_get(ta_ctx* ctx, int block_size, ta_schedule_view* out);
 

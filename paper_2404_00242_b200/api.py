@@ -166,10 +166,47 @@ class TreeAttention:
         check(lib().ta_pool_token_ref(self._h, int(node), int(token), C.byref(p), C.byref(s)), "token_ref")
         return p.value, s.value
 
+    # ------------------------------------------------------------ checking
+    def _torch_dtype(self, name):
+        import torch
+        return torch.bfloat16 if name in ("bf16", "bfloat16") else torch.float32
+
+    def _check_buf(self, what, x, shape, dtype_name, device_only=True):
+        """Layout contract of the C ABI: dense row-major, the context's dtype,
+        the context's device.  A mismatch is the reference's invalid_argument."""
+        if x is None:
+            return
+        if hasattr(x, "is_contiguous"):   # torch
+            want = self._torch_dtype(dtype_name)
+            if x.dtype != want:
+                raise ValueError(f"{what}: dtype {x.dtype}, expected {want}")
+            if not x.is_contiguous():
+                raise ValueError(f"{what}: tensor must be contiguous")
+            if device_only and (not x.is_cuda or x.device.index != self.device):
+                raise ValueError(f"{what}: must be a tensor on cuda:{self.device}, got {x.device}")
+            if not device_only and x.is_cuda and x.device.index != self.device:
+                raise ValueError(f"{what}: on {x.device}, context is on cuda:{self.device}")
+        elif isinstance(x, np.ndarray):
+            if device_only:
+                raise ValueError(f"{what}: expected a device tensor, got a numpy array")
+            if not x.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"{what}: array must be C-contiguous")
+            isz = 2 if dtype_name in ("bf16", "bfloat16") else 4
+            if x.dtype.itemsize != isz:
+                raise ValueError(f"{what}: element size {x.dtype.itemsize}, expected {isz} ({dtype_name})")
+        else:
+            return   # raw pointer: the caller vouches for the layout
+        if tuple(x.shape) != tuple(shape) and int(np.prod(x.shape)) != int(np.prod(shape)):
+            raise ValueError(f"{what}: shape {tuple(x.shape)}, expected {tuple(shape)}")
+
     def write_kv(self, layer: int, node: int, k, v, tok_begin: int = 0, stream=None):
         """k, v: [n_tok][n_local_kv_heads][d_head] (torch device tensor or host numpy/torch)."""
         n = int(k.shape[0])
         on_dev = bool(getattr(k, "is_cuda", False))
+        for nm, x in (("write_kv k", k), ("write_kv v", v)):
+            self._check_buf(nm, x, (n, self.n_local_kv_heads, self.d_head), self.kv_dtype, device_only=False)
+        if bool(getattr(v, "is_cuda", False)) != on_dev:
+            raise ValueError("write_kv: k and v must both be on the device or both on the host")
         check(lib().ta_kv_write(self._h, int(layer), int(node), int(tok_begin), n, _ptr(k), _ptr(v),
                                 int(on_dev), _stream(stream)), "write_kv")
 
@@ -203,10 +240,21 @@ class TreeAttention:
 
     def attend(self, layer: int, q, out=None, lse=None, stream=None):
         """q [L][n_local_q_heads][d_head] device tensor -> out (same layout)."""
+        L = int(q.shape[0]) if hasattr(q, "shape") else None
+        if L is not None:
+            n = C.c_int()
+            check(lib().ta_tree_leaves(self._h, None, 0, C.byref(n)), "leaves")
+            if L != n.value:
+                raise ValueError(f"attend q: {L} query rows, the tree has {n.value} leaves")
+            shape = (L, self.n_local_q_heads, self.d_head)
+            self._check_buf("attend q", q, shape, self.kv_dtype)
         if out is None:
             import torch
-            dt = torch.float32 if self.out_dtype in ("f32", "float32") else torch.bfloat16
-            out = torch.empty(q.shape, dtype=dt, device=q.device)
+            out = torch.empty(shape, dtype=self._torch_dtype(self.out_dtype), device=q.device)
+        elif L is not None:
+            self._check_buf("attend out", out, shape, self.out_dtype)
+        if lse is not None and L is not None:
+            self._check_buf("attend lse", lse, (L, self.n_local_q_heads), "f32")
         check(lib().ta_attend(self._h, int(layer), _ptr(q), _ptr(out), _ptr(lse), _stream(stream)), "attend")
         return out
 
@@ -253,7 +301,7 @@ class TreeAttention:
                 "merge_leaf": arr(v.merge_leaf, v.n_merge), "merge_head": arr(v.merge_head, v.n_merge),
                 "merge_begin": arr(v.merge_begin, v.n_merge + 1), "merge_parts": arr(v.merge_parts, n_mp),
                 "empty": arr(v.empty, 2 * v.n_empty).reshape(-1, 2), "n_lanes": v.n_lanes,
-                "use_mma": bool(v.use_mma)}
+                "use_mma": bool(v.use_mma), "fused_merge": bool(v.fused_merge)}
 
     def launches_per_attend(self) -> int:
         return lib().ta_launches_per_attend(self._h)

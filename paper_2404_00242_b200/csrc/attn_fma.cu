@@ -372,13 +372,8 @@ __global__ void __launch_bounds__(256, 1) attn_fma_kernel(const AttnArgs a) {
 template <typename T, int D, int R>
 cudaError_t launch_fma_t(const AttnArgs& a, bool pdl, cudaStream_t s) {
     constexpr size_t smem = fma_smem_bytes<T, D, R>();
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e =
-            cudaFuncSetAttribute(attn_fma_kernel<T, D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = set_smem_attr_once((const void*)attn_fma_kernel<T, D, R>, (int)smem);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(a.n_ctas);
     cfg.blockDim = dim3(256);
@@ -395,6 +390,7 @@ cudaError_t launch_fma_t(const AttnArgs& a, bool pdl, cudaStream_t s) {
 template <typename T, int R>
 cudaError_t launch_fma_d(const AttnArgs& a, bool pdl, cudaStream_t s) {
     switch (a.D) {
+        case 8: return launch_fma_t<T, 8, R>(a, pdl, s);
         case 16: return launch_fma_t<T, 16, R>(a, pdl, s);
         case 32: return launch_fma_t<T, 32, R>(a, pdl, s);
         case 64: return launch_fma_t<T, 64, R>(a, pdl, s);

@@ -17,14 +17,22 @@
 //                   O rescale; pass 2: tcgen05.ld S -> P = exp2 -> bf16 ->
 //                   tcgen05.st into TMEM.  Warps none of whose rows attend
 //                   the tile (sparse lanes) skip the exponentials.
-// TMEM: S0 [0,128) S1 [128,256) O [256,384) P [384,448) Q [448,512); the
-// whole SMEM budget goes to the KV ring.
-// At an item's end the softmax warps write each attended row either as the
-// final output (its leaf-head is covered by this item alone) or as an
-// (O/l, log2 lse) partial record that merge.cu combines right after.
+// TMEM: S0 [0,128) S1 [128,256) O [256,384) Q0 [384,448) Q1 [448,512) (Q
+// double-buffered by item parity; P aliased into the S buffer it came from).
+// At an item's end the softmax warps write each attended row as
+//   * the final output, when this item covers its leaf-head alone;
+//   * an (O/l, log2 lse) partial record, published to the leaf-head's merge
+//     counter once its bulk copy has landed (deferred by about a tile);
+//   * or, for the leaf-head's LAST item (fused merge), the merge itself: wait
+//     until the earlier items' partials are published, fold them with the
+//     on-chip share in item order, write the output.  Waits only ever point
+//     to earlier positions of the (head, lane, tile) sequence, i.e. to CTAs
+//     that are resident or done, so the grid (<= one CTA per SM) cannot
+//     deadlock.  Schedules that cannot guarantee co-residency use merge.cu.
 //
 // Reference semantics: group_attention (attention.hpp:117-204) over every
-// chunk a leaf attends; tree_reduce (attention.hpp:209-233) in merge.cu.
+// chunk a leaf attends; tree_reduce (attention.hpp:209-233) in the owner's
+// epilogue (or merge.cu).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -80,7 +88,8 @@ enum { FULLK = 0, FULLV = NSTAGE, EMPTYK = 2 * NSTAGE, EMPTYV = 3 * NSTAGE, S_FU
 constexpr int TMEM_SLOT = 240;                           // offset of the TMEM address in the barrier block
 static_assert(NBAR * 8 <= TMEM_SLOT, "barriers overlap the TMEM slot");
 
-// Optional pipeline trace (debug; AttnArgs::trace != nullptr): per CTA 256
+// Optional pipeline trace (a separate TRACE=true instantiation, launched only
+// when AttnArgs::trace or ::timeline is set): per CTA 256
 // int64 slots: [0] start / [1] end (%globaltimer ns), [2] SM id, [3] tiles, [4] / [5] clock64 at start / end,
 // then per tile t < 27 (clock64, 8 slots): [8+8t] K loads issued, [+1] S
 // seen by softmax, [+2] S loaded + masked, [+3] row max exchanged, [+4]
@@ -97,21 +106,51 @@ __device__ __forceinline__ long long gtimer() {
 // 224 + w: softmax warp w's last epilogue end; 232 + c: O columns c loaded
 #define TA_TRACE_EPI(a, item, k)                                                                   \
     do {                                                                                           \
-        if ((a).trace && threadIdx.x == TRACE_TID) {                                               \
-            if ((item) == 0) (a).trace[blockIdx.x * TRACE_SLOTS + 240 + (k)] = clock64();          \
-            (a).trace[blockIdx.x * TRACE_SLOTS + 248 + (k)] = clock64();                           \
+        if constexpr (TRACE) {                                                                     \
+            if ((a).trace && threadIdx.x == TRACE_TID) {                                           \
+                if ((item) == 0) (a).trace[blockIdx.x * TRACE_SLOTS + 240 + (k)] = clock64();      \
+                (a).trace[blockIdx.x * TRACE_SLOTS + 248 + (k)] = clock64();                       \
+            }                                                                                      \
         }                                                                                          \
     } while (0)
 #define TA_TRACE(a, t, k)                                                                          \
     do {                                                                                           \
-        if ((a).trace && (t) < TRACE_TILES) (a).trace[blockIdx.x * TRACE_SLOTS + 8 + 8 * (t) + (k)] = clock64(); \
+        if constexpr (TRACE) {                                                                     \
+            if ((a).trace && (t) < TRACE_TILES) (a).trace[blockIdx.x * TRACE_SLOTS + 8 + 8 * (t) + (k)] = clock64(); \
+        }                                                                                          \
     } while (0)
+
+// ---- fused merge: publication of partial records and the owner's wait
+// A thread's partial row-half is published once its bulk copy has completed:
+// async-proxy writes -> proxy fence -> release -> counter increment.
+__device__ __forceinline__ void publish_partial(unsigned* cnt) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Spin until `target` pieces are in.  A schedule bug must fail loudly, not
+// hang the GPU: trap after 2 s.
+__device__ __forceinline__ void wait_pieces(const unsigned* cnt, unsigned target) {
+    if (ld_acquire(cnt) >= target) return;
+    const long long t0 = gtimer();
+    while (ld_acquire(cnt) < target) {
+        __nanosleep(128);
+        if (gtimer() - t0 > 2000000000LL) __trap();
+    }
+}
 
 struct TmapSet {
     CUtensorMap k[4];   // boxes of 16, 32, 64, 128 pool rows x 64 columns
     CUtensorMap v[4];
 };
 
+template <bool TRACE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_mma_kernel(const __grid_constant__ TmapSet tm, const AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
@@ -124,7 +163,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     float* redl = reinterpret_cast<float*>(smem + SMEM_REDL);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0 && a.timeline) {   // debug: CTA entry (first / last over the grid)
+    if (TRACE && threadIdx.x == 0 && a.timeline) {   // debug: CTA entry (first / last over the grid)
         timeline_mark(a.timeline, 4, true);
         timeline_mark(a.timeline, 4, false);
     }
@@ -200,7 +239,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncthreads();
     const uint32_t tmem = *tmem_slot;
-    if (threadIdx.x == 0 && a.timeline) {   // debug: schedule staged
+    if (TRACE && threadIdx.x == 0 && a.timeline) {   // debug: schedule staged
         timeline_mark(a.timeline, 6, true);
         timeline_mark(a.timeline, 6, false);
     }
@@ -221,7 +260,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tma_prefetch_2d(&tm.v[sz], 64, row);
         }
     }
-    if (warp >= SOFT0 && n_items > 0 && !(a.debug & 8)) {
+    if (warp >= SOFT0 && n_items > 0) {
         const int r = (warp & 3) * 32 + lane, h = (warp - SOFT0) >> 2;
         const ItemDesc I0 = s_item[0];
         if (r < I0.n_slots * a.G && r / a.G < ns_s) {
@@ -231,8 +270,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     }
     pdl_wait();   // previous launch finished: queries, outputs, partial scratch are ours
-    if (threadIdx.x == 0) timeline_mark(a.timeline, 0, true);
-    if (a.trace && threadIdx.x == 0) {
+    if (TRACE && threadIdx.x == 0) timeline_mark(a.timeline, 0, true);
+    if (TRACE && a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS] = gtimer();
         a.trace[blockIdx.x * TRACE_SLOTS + 4] = clock64();
         unsigned smid;
@@ -379,6 +418,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             q_store(qv, 0);
         }
         int gt = 0;
+        int pend = -1;   // merge record of this thread's last partial, not yet published (fused merge)
         for (int k = 0; k < n_items; ++k) {
             const ItemDesc I = item_at(k);
             const int nrows = I.n_slots * G;
@@ -391,20 +431,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // buffer during this item's first tile (L2-prefetched before it)
             const bool has_next = k + 1 < n_items;
             const int code = live_row ? a.slot_out[I.out_begin + j] : kSlotUnused;
-            if ((a.debug & 4) && code != kSlotUnused) {
-                // warm L2 with the lines this row's epilogue writes (no fill under load)
-                const char* dst = code >= 0 ? reinterpret_cast<const char*>(a.part_o + ((size_t)code * G + g_in) * DH + 64 * h)
-                                            : reinterpret_cast<const char*>(a.out) +
-                                                  (((size_t)(-1 - code) * a.hq_loc + I.head * G + g_in) * DH + 64 * h) *
-                                                      (a.out_bf16 ? 2 : 4);
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(dst));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(dst + 128));
-            }
             int nleaf = -1;
             if (has_next) {
                 const ItemDesc In = item_at(k + 1);
                 nleaf = r < In.n_slots * G ? leaf_at(k + 1, In, r / G) : -1;
-                if (nleaf >= 0 && !(a.debug & 2)) asm volatile("prefetch.global.L2 [%0];" ::"l"(q_row(In, nleaf)));
+                if (nleaf >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(q_row(In, nleaf)));
             }
 
             for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
@@ -519,6 +550,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     tc_fence_after();
                     q_store(qv, (k + 1) & 1);
                 }
+                if (pend >= 0 && t == I.tile_begin + 1) {
+                    // the previous item's partial has had a tile to land: publish it
+                    publish_partial(a.merge_cnt + pend);
+                    pend = -1;
+                }
             }
 
             // ---- epilogue
@@ -530,37 +566,63 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             named_bar(1 + q4, 64);
             l += redl[(h ^ 1) * BM + r];
             TA_TRACE_EPI(a, k, 4);
+            // an unpublished partial of the previous item goes out before this
+            // item may wait on anyone (deadlock freedom of the fused merge)
+            if (pend >= 0) {
+                publish_partial(a.merge_cnt + pend);
+                pend = -1;
+            }
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            const float lse2 = m + log2f(l);
+            float lse2 = m + log2f(l);
+            // fused merge (owner rows): fold the earlier items' partials in item
+            // order, then this item's share; weights relative to the common max
+            const bool owner = code >= kOwnerBase;
+            int4 rec = make_int4(0, 0, 0, 0);
+            float s_own = inv;
+            if (owner) {
+                rec = __ldg(a.merge_rec + (code - kOwnerBase));
+                wait_pieces(a.merge_cnt + (code - kOwnerBase), (unsigned)(rec.w * 2 * G));
+                float M = lse2;
+                for (int p = 0; p < rec.w; ++p) M = fmaxf(M, __ldcg(a.part_lse + (size_t)(rec.z + p) * G + g_in));
+                float den = ex2(lse2 - M);
+                for (int p = 0; p < rec.w; ++p) den += ex2(__ldcg(a.part_lse + (size_t)(rec.z + p) * G + g_in) - M);
+                s_own = ex2(lse2 - M) * inv / den;
+                lse2 = M + log2f(den);
+            }
             if (code != kSlotUnused && h == 0) {
-                if (code < 0) {
-                    if (a.lse) a.lse[(size_t)(-1 - code) * a.hq_loc + I.head * G + g_in] = lse2 * kLn2;
+                if (code < 0 || owner) {
+                    const int leaf = owner ? rec.x : -1 - code;
+                    if (a.lse) a.lse[(size_t)leaf * a.hq_loc + I.head * G + g_in] = lse2 * kLn2;
                 } else {
                     a.part_lse[(size_t)code * G + g_in] = lse2;
                 }
             }
             if (warp_live) {
-                // O / l -> this thread's staging row (its TMEM lane = output row,
-                // its 64 columns), then one bulk async copy of the row to the
+                // O (scaled) -> this thread's staging row (its TMEM lane = output
+                // row, its 64 columns), then one bulk async copy of the row to the
                 // final output or the partial record: the stores drain in the
                 // background instead of stalling the softmax warps behind the
                 // saturated read stream.  Compact loops: this code runs once per
                 // item, I-cache cold.
                 const uint32_t srow = sbase + SMEM_EPI + (uint32_t)(((warp - SOFT0) * 32 + lane) * EPI_ROW);
-                const bool st_bf16 = code < 0 && a.out_bf16;
+                const bool out_final = code < 0 || owner;
+                const bool st_bf16 = out_final && a.out_bf16;
                 // the row's previous bulk copy (an earlier item) has read the staging
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 TA_TRACE_EPI(a, k, 3);
+                const bool stage_f32 = !st_bf16 || owner;   // owners accumulate in fp32 first
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     uint32_t o[16];
                     TA_TMEM_LD16(tmem + lane_addr + TMEM_O + h * 64 + c * 16, o);
                     tmem_wait_ld();
-                    if (a.trace && threadIdx.x == TRACE_TID) a.trace[blockIdx.x * TRACE_SLOTS + 232 + c] = clock64();
+                    if constexpr (TRACE) {
+                        if (a.trace && threadIdx.x == TRACE_TID) a.trace[blockIdx.x * TRACE_SLOTS + 232 + c] = clock64();
+                    }
                     float f[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(o[i]) * inv;
-                    if (st_bf16) {
+                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(o[i]) * s_own;
+                    if (!stage_f32) {
                         sts128(srow + (uint32_t)(c * 32), pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]),
                                pack_bf16(f[6], f[7]));
                         sts128(srow + (uint32_t)(c * 32 + 16), pack_bf16(f[8], f[9]), pack_bf16(f[10], f[11]),
@@ -572,32 +634,74 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                    __float_as_uint(f[4 * q + 2]), __float_as_uint(f[4 * q + 3]));
                     }
                 }
-                if (code != kSlotUnused && !(a.debug & 1)) {
-                    void* dst = code >= 0 ? static_cast<void*>(a.part_o + ((size_t)code * G + g_in) * DH + 64 * h)
-                                          : static_cast<void*>(reinterpret_cast<char*>(a.out) +
-                                                               (((size_t)(-1 - code) * a.hq_loc + I.head * G + g_in) * DH + 64 * h) *
-                                                                   (a.out_bf16 ? 2 : 4));
+                if (owner) {
+                    const float M = lse2;   // final lse: w_p / den = 2^(lse_p - lse)
+#pragma unroll 1
+                    for (int p = 0; p < rec.w; ++p) {
+                        const size_t pid = (size_t)(rec.z + p);
+                        const float w = ex2(__ldcg(a.part_lse + pid * G + g_in) - M);
+                        const float4* src = reinterpret_cast<const float4*>(a.part_o + (pid * G + g_in) * DH + 64 * h);
+#pragma unroll 1
+                        for (int hh = 0; hh < 16; hh += 8) {
+                        float4 v[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) v[i] = __ldcg(src + hh + i);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const uint32_t sa = srow + 16u * (hh + i);
+                            float4 x = lds128f(sa);
+                            x.x = fmaf(w, v[i].x, x.x);
+                            x.y = fmaf(w, v[i].y, x.y);
+                            x.z = fmaf(w, v[i].z, x.z);
+                            x.w = fmaf(w, v[i].w, x.w);
+                            sts128(sa, __float_as_uint(x.x), __float_as_uint(x.y), __float_as_uint(x.z), __float_as_uint(x.w));
+                        }
+                        }
+                    }
+                    if (st_bf16) {   // fp32 staging -> bf16 in place (first 128 bytes, front to back)
+#pragma unroll 1
+                        for (int i = 0; i < 8; ++i) {
+                            const float4 x0 = lds128f(srow + 32u * i), x1 = lds128f(srow + 32u * i + 16u);
+                            sts128(srow + 16u * i, pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y),
+                                   pack_bf16(x1.z, x1.w));
+                        }
+                    }
+                    // the record's counter is ours alone now: the last of its 2G
+                    // readers resets it for the next launch
+                    const unsigned target = (unsigned)(rec.w * 2 * G);
+                    if (atomicAdd(a.merge_cnt + (code - kOwnerBase), 1u) == target + 2u * G - 1u)
+                        a.merge_cnt[code - kOwnerBase] = 0u;
+                }
+                if (code != kSlotUnused) {
+                    const int leaf = owner ? rec.x : -1 - code;
+                    void* dst = !out_final ? static_cast<void*>(a.part_o + ((size_t)code * G + g_in) * DH + 64 * h)
+                                           : static_cast<void*>(reinterpret_cast<char*>(a.out) +
+                                                                (((size_t)leaf * a.hq_loc + I.head * G + g_in) * DH + 64 * h) *
+                                                                    (a.out_bf16 ? 2 : 4));
                     fence_proxy_async();   // the staging writes -> visible to the bulk copy
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(srow),
                                  "r"(st_bf16 ? 128u : 256u)
                                  : "memory");
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    if (!out_final && a.fused_merge) pend = __ldg(a.part_merge + code);
                 }
             }
             TA_TRACE_EPI(a, k, 2);
             tc_fence_before();
             if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt - 1, 7);
-            if (a.trace && lane == 0) a.trace[blockIdx.x * TRACE_SLOTS + 224 + warp - SOFT0] = clock64();
+            if constexpr (TRACE) {
+                if (a.trace && lane == 0) a.trace[blockIdx.x * TRACE_SLOTS + 224 + warp - SOFT0] = clock64();
+            }
         }
-
+        if (pend >= 0) publish_partial(a.merge_cnt + pend);
     }
 
     // the epilogues' bulk copies are complete (writes performed) before exit
     if (warp >= SOFT0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tc_fence_before();
     __syncthreads();
-    if (threadIdx.x == 0) timeline_mark(a.timeline, 0, false);
-    if (a.trace && threadIdx.x == 0) {
+    if (TRACE && threadIdx.x == 0) timeline_mark(a.timeline, 0, false);
+    if (TRACE && a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS + 1] = gtimer();
         a.trace[blockIdx.x * TRACE_SLOTS + 5] = clock64();
         int nt = 0;
@@ -637,12 +741,10 @@ bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D, int b
 
 cudaError_t launch_attn_mma(const AttnArgs& a, bool pdl, cudaStream_t s) {
     if (!mma_supported(a.D, a.kv_bf16)) return cudaErrorNotSupported;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    const bool trace = a.trace || a.timeline;
+    cudaError_t e = set_smem_attr_once(trace ? (const void*)attn_mma_kernel<true> : (const void*)attn_mma_kernel<false>,
+                                       SMEM_BYTES);
+    if (e != cudaSuccess) return e;
     TmapSet tm;
     std::memcpy(tm.k, a.tmap_k, sizeof(tm.k));
     std::memcpy(tm.v, a.tmap_v, sizeof(tm.v));
@@ -656,7 +758,8 @@ cudaError_t launch_attn_mma(const AttnArgs& a, bool pdl, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, attn_mma_kernel, tm, a);
+    return trace ? cudaLaunchKernelEx(&cfg, attn_mma_kernel<true>, tm, a)
+                 : cudaLaunchKernelEx(&cfg, attn_mma_kernel<false>, tm, a);
 }
 
 }  // namespace ta

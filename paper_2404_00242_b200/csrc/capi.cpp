@@ -62,10 +62,12 @@ struct ta_ctx {
     const int4* d_merge_rec = nullptr;
     const int32_t* d_part_merge = nullptr;
     const int32_t* d_empty = nullptr;
+    unsigned* merge_cnt = nullptr;   // fused merge counters, one per merge record
+    size_t merge_cnt_cap = 0;        // bytes
+    bool fused_merge = true;         // option "fused_merge"
     bool pdl = true;
     int prefetch_tiles = 2;
     int64_t trace = 0;  // debug: device buffer for the MMA kernel's pipeline trace
-    int debug = 0;      // debug experiment bits
     int64_t timeline = 0;   // debug: per-launch start/end timestamps
     int num_sms = 148;
 
@@ -105,6 +107,7 @@ struct ta_ctx {
             cudaFree(meta_dev);
             cudaFreeHost(meta_host);
             cudaFree(part);
+            cudaFree(merge_cnt);
             cudaFree(stage_dev);
             cudaFreeHost(stage_host);
             cudaFree(io_dev);
@@ -203,8 +206,8 @@ ta_status ta_ctx_create(int device, const ta_shape* s, ta_ctx** out) {
             fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: bad kv head shard");
         if ((sh.kv_dtype != TA_F32 && sh.kv_dtype != TA_BF16) || (sh.out_dtype != TA_F32 && sh.out_dtype != TA_BF16))
             fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: dtype must be TA_F32 or TA_BF16");
-        if (device >= 0 && sh.d_head != 16 && sh.d_head != 32 && sh.d_head != 64 && sh.d_head != 128)
-            fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: d_head must be 16, 32, 64 or 128 on the device");
+        if (device >= 0 && sh.d_head != 8 && sh.d_head != 16 && sh.d_head != 32 && sh.d_head != 64 && sh.d_head != 128)
+            fail(TA_ERR_INVALID_ARGUMENT, "ta_ctx_create: d_head must be 8, 16, 32, 64 or 128 on the device");
         auto c = std::make_unique<ta_ctx>();
         c->shape = sh;
         c->G = sh.n_q_heads / sh.n_kv_heads;
@@ -226,6 +229,11 @@ ta_status ta_ctx_create(int device, const ta_shape* s, ta_ctx** out) {
             const size_t bytes = (size_t)c->layer_elems * sh.n_layers * c->esize;
             cuda_check(cudaMalloc(&c->kv_k, bytes), "cudaMalloc(K pool)");
             cuda_check(cudaMalloc(&c->kv_v, bytes), "cudaMalloc(V pool)");
+            // Zeroed once: the tcgen05 kernel loads whole 16-row boxes, so the
+            // unwritten tail rows of a node's last page are read too.  Their P is
+            // exactly 0, but 0 * NaN would poison O if reused memory held NaNs.
+            cuda_check(cudaMemset(c->kv_k, 0, bytes), "cudaMemset(K pool)");
+            cuda_check(cudaMemset(c->kv_v, 0, bytes), "cudaMemset(V pool)");
             cuda_check(cudaEventCreateWithFlags(&c->meta_done, cudaEventDisableTiming), "cudaEventCreate");
             cudaDeviceProp prop;
             cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
@@ -295,13 +303,13 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->timeline = v;
         } else if (k == "trace_ptr") {
             c->trace = v;
-        } else if (k == "debug") {
-            c->debug = (int)v;
+        } else if (k == "fused_merge") {
+            c->fused_merge = v != 0;
         } else {
             fail(TA_ERR_INVALID_ARGUMENT, "unknown option " + k);
         }
         // launch-only knobs keep the prepared schedule
-        if (k != "trace_ptr" && k != "timeline_ptr" && k != "debug" && k != "pdl" && k != "prefetch_tiles")
+        if (k != "trace_ptr" && k != "timeline_ptr" && k != "pdl" && k != "prefetch_tiles")
             c->prepared = false;
     });
 }
@@ -322,6 +330,14 @@ ta_status ta_tree_restore(ta_ctx* c, int32_t root, int n, const int32_t* ids, co
         // validate on a scratch tree first so a bad snapshot leaves ctx intact
         Tree probe;
         probe.restore(root, n, ids, parents, counts);
+        // ... and check the page demand before the pool is reset
+        if (c->pool.capacity >= 0) {
+            int64_t need = 0;
+            for (int i = 0; i < n; ++i) need += (counts[i] + c->pool.page_size - 1) / c->pool.page_size;
+            if (need > c->pool.capacity)
+                fail(TA_ERR_OUT_OF_MEMORY, "restore: snapshot needs " + std::to_string(need) + " pages, capacity is " +
+                                               std::to_string(c->pool.capacity));
+        }
         c->pool.reset();
         c->tree.restore(root, n, ids, parents, counts);
     });
@@ -408,6 +424,9 @@ ta_status ta_kv_write(ta_ctx* c, int layer, int32_t node, int64_t t0, int64_t n,
         if (t0 < 0 || n < 0 || t0 + n > h.n_tokens)
             fail(TA_ERR_INVALID_ARGUMENT, "write_kv: token index out of range");
         if (n == 0) return;
+        if (!k || !v) fail(TA_ERR_INVALID_ARGUMENT, "write_kv: null key/value");
+        if (src_on_device && (((uintptr_t)k | (uintptr_t)v) & 15))
+            fail(TA_ERR_INVALID_ARGUMENT, "write_kv: device key/value rows must be 16-byte aligned");
         cudaStream_t s = (cudaStream_t)stream;
         cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
         const int P = c->pool.page_size;
@@ -482,8 +501,18 @@ SchedOptions effective_opts(const ta_ctx* c) {
     SchedOptions o = c->opt;
     o.use_mma = o.use_mma && mma_supported(c->shape.d_head, c->shape.kv_dtype == TA_BF16);
     if (!o.use_mma) o.tile_groups = fma_tile_groups(c->shape.d_head, c->esize);
+    // The merge runs inside the tcgen05 launch when every CTA can be resident
+    // at once (one CTA per SM): a record's last item then waits only for
+    // items of earlier CTAs, which are running or done.
+    o.fused_merge = o.use_mma && c->fused_merge && o.num_ctas <= c->num_sms;
     return o;
 }
+
+// Row capacity of the FMA kernel instantiation for a schedule whose widest
+// lane has `rows` rows (a lane always holds whole GQA groups: rows <= max(G,
+// fma_max_rows)).  ta_prepare rejects G > kFmaMaxRows on the FMA path.
+constexpr int kFmaMaxRows = 16;
+int fma_rows(int rows) { return rows <= 4 ? 4 : rows <= 8 ? 8 : 16; }
 
 }  // namespace
 
@@ -498,6 +527,13 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         c->plan_version = c->tree.version;
         c->plan_bs = bs;
         const SchedOptions o = effective_opts(c);
+        // a lane holds whole GQA groups: the kernels' row capacity bounds G
+        if (o.use_mma && c->G > 128)
+            fail(TA_ERR_INVALID_ARGUMENT, "prepare: GQA group size " + std::to_string(c->G) +
+                                              " exceeds the tensor-core kernel's 128 rows");
+        if (!o.use_mma && c->G > kFmaMaxRows)
+            fail(TA_ERR_INVALID_ARGUMENT, "prepare: GQA group size " + std::to_string(c->G) +
+                                              " exceeds the FMA kernel's 16 rows (use bf16 KV with d_head 128)");
         build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, o, c->sched);
         const Schedule& S = c->sched;
         struct Part {
@@ -547,6 +583,14 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         c->d_merge_rec = (const int4*)(d + parts[8].off);
         c->d_part_merge = (const int32_t*)(d + parts[9].off);
         c->d_empty = (const int32_t*)(d + parts[12].off);
+        // fused-merge counters: zero at every prepare (self-resetting in the kernel)
+        const size_t cb = sizeof(unsigned) * std::max<size_t>(1, S.merge_rec.size());
+        if (cb > c->merge_cnt_cap) {
+            void* p = c->merge_cnt;
+            grow_dev(&p, &c->merge_cnt_cap, cb);
+            c->merge_cnt = (unsigned*)p;
+        }
+        cuda_check(cudaMemsetAsync(c->merge_cnt, 0, cb, s), "cudaMemsetAsync(merge counters)");
         // partial scratch: o [n_part][G][D] + lse [n_part][G]
         const size_t pf = (size_t)std::max(1, S.n_partials) * c->G * (c->shape.d_head + 1);
         if (pf > c->part_cap) {
@@ -592,6 +636,8 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.merge_rec = c->d_merge_rec;
     a.part_merge = c->d_part_merge;
     a.n_merge = (int)S.merge_rec.size();
+    a.merge_cnt = c->merge_cnt;
+    a.fused_merge = S.fused_merge ? 1 : 0;
     a.empty = c->d_empty;
     a.n_empty = (int)(S.empty.size() / 2);
     a.n_ctas = (int)S.cta_begin.size() - 1;
@@ -602,20 +648,19 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.kv_bf16 = c->shape.kv_dtype == TA_BF16;
     a.out_bf16 = c->shape.out_dtype == TA_BF16;
     a.trace = reinterpret_cast<long long*>(c->trace);
-    a.debug = c->debug;
     a.timeline = reinterpret_cast<unsigned long long*>(c->timeline);
     a.prefetch_tiles = c->prefetch_tiles;
 
     const SchedOptions o = effective_opts(c);
-    if (o.use_mma && (((uintptr_t)out | (uintptr_t)q) & 15))
-        fail(TA_ERR_INVALID_ARGUMENT, "attend: q and out must be 16-byte aligned");
-    // merge inside the attention launch when every CTA is resident at once
-    // (the merging CTAs wait on the producing ones); else a merge launch
+    // both kernels move q / out / lse rows in 16-byte units
+    if (!q || !out) fail(TA_ERR_INVALID_ARGUMENT, "attend: null q or out");
+    if (((uintptr_t)out | (uintptr_t)q) & 15) fail(TA_ERR_INVALID_ARGUMENT, "attend: q and out must be 16-byte aligned");
+    cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
     if (o.use_mma)
         cuda_check(launch_attn_mma(a, c->pdl, s), "attn_mma");
     else
-        cuda_check(launch_attn_fma(a, std::min(o.fma_max_rows, std::max(1, S.max_lane_rows)), c->pdl, s), "attn_fma");
-    cuda_check(launch_merge(a, a.n_merge, c->pdl, s), "merge");
+        cuda_check(launch_attn_fma(a, fma_rows(S.max_lane_rows), c->pdl, s), "attn_fma");
+    if (!S.fused_merge) cuda_check(launch_merge(a, a.n_merge, c->pdl, s), "merge");
 }
 
 ta_status ta_attend(ta_ctx* c, int layer, const void* q, void* out, float* lse, void* stream) {
@@ -750,12 +795,13 @@ ta_status ta_schedule_get(ta_ctx* c, int bs, ta_schedule_view* o) {
         o->empty = S.empty.data();
         o->n_lanes = S.n_lanes;
         o->use_mma = effective_opts(c).use_mma ? 1 : 0;
+        o->fused_merge = S.fused_merge ? 1 : 0;
     });
 }
 
 int ta_launches_per_attend(ta_ctx* c) {
     if (!c || !c->prepared) return 0;
-    return 1 + (c->sched.merge_leaf.empty() ? 0 : 1);
+    return 1 + (c->sched.merge_leaf.empty() || c->sched.fused_merge ? 0 : 1);
 }
 
 }  // extern "C"

@@ -138,16 +138,32 @@ std::vector<int32_t> Tree::branch(int32_t at, const int64_t* counts, int n) {
         if (counts[i] < 0) fail(TA_ERR_INVALID_ARGUMENT, "branch: negative child token count");
     reserve(next_id + n + 1);
     std::vector<int32_t> created;
-    for (int i = 0; i < n; ++i) {
-        const int32_t id = next_id++;
-        alive[id] = 1;
-        parent[id] = at;
-        count[id] = counts[i];
-        kids[id].clear();
-        kids[at].push_back(id);
-        created.push_back(id);
-        ++n_alive;
-        if (hook) hook->on_alloc(id, counts[i]);
+    const int32_t first_id = next_id;
+    try {
+        for (int i = 0; i < n; ++i) {
+            const int32_t id = next_id;
+            if (hook) hook->on_alloc(id, counts[i]);   // atomic: allocates all of the child's pages or none
+            ++next_id;
+            alive[id] = 1;
+            parent[id] = at;
+            count[id] = counts[i];
+            kids[id].clear();
+            kids[at].push_back(id);
+            created.push_back(id);
+            ++n_alive;
+        }
+    } catch (...) {
+        // a bounded device pool ran out part way: undo the children created so
+        // far, so the tree and the pool stay consistent (the reference's pool is
+        // unbounded and never gets here)
+        for (int32_t id : created) {
+            if (hook) hook->on_free(id);
+            alive[id] = 0;
+            --n_alive;
+        }
+        kids[at].clear();
+        next_id = first_id;
+        throw;
     }
     rebuild();
     return created;
@@ -215,13 +231,27 @@ void PagePool::allocate(int32_t node, int64_t n) {
     if (n < 0) fail(TA_ERR_INVALID_ARGUMENT, "allocate: negative token count");
     if (handles.count(node)) fail(TA_ERR_LOGIC, "allocate: node already has a handle");
     handles.emplace(node, Handle{});
-    extend(node, n);
+    try {
+        extend(node, n);
+    } catch (...) {
+        handles.erase(node);
+        throw;
+    }
 }
 
 void PagePool::extend(int32_t node, int64_t n) {
     auto it = handles.find(node);
     if (it == handles.end()) fail(TA_ERR_LOGIC, "extend: no handle for node");
     Handle& h = it->second;
+    if (capacity >= 0) {   // all or nothing: check the page demand before taking any
+        const int64_t room = h.pages.empty() ? 0 : page_size - pages[h.pages.back()].used;
+        const int64_t need = n > room ? (n - room + page_size - 1) / page_size : 0;
+        const int64_t avail = (int64_t)free_list.size() + capacity - (int64_t)pages.size();
+        if (need > avail)
+            fail(TA_ERR_OUT_OF_MEMORY, "PagePool: device page capacity exhausted (" + std::to_string(capacity) +
+                                           " pages, " + std::to_string(need) + " more needed, " + std::to_string(avail) +
+                                           " free)");
+    }
     // Fill this node's tail page first; never share a page across nodes.
     while (n > 0) {
         if (!h.pages.empty()) {
@@ -428,8 +458,9 @@ std::string plan_json(const Tree& t, const Plan& p) {
 //    contiguous runs of equal cost (box rows + a fixed per-tile cost); each
 //    run's maximal (head, lane) pieces are its items.
 // 4. Outputs.  A leaf-head attended by one item is written directly; else
-//    every item writes a partial and the last one to finish merges them in
-//    item order (tree_reduce, attention.hpp:209-233).
+//    its items write partials that are merged in item order (tree_reduce,
+//    attention.hpp:209-233): by the leaf-head's last item inside the attention
+//    launch (fused merge, tcgen05 kernel) or by the merge launch after it.
 // ===========================================================================
 namespace {
 
@@ -785,12 +816,27 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
             }
         }
     }
-    // partial ids are contiguous per merge record (record mi owns ids
-    // [merge_begin[mi], merge_begin[mi+1]) in item order), so the merge reads
-    // them without an id list
+    // Partial ids are contiguous per merge record (record mi owns ids
+    // [merge_begin[mi], merge_begin[mi+1]) in item order), so a merge reads
+    // them without an id list.  Fused merge: the record's LAST item (largest
+    // position in the (head, lane, tile) sequence) keeps its share on chip,
+    // waits for the others' partials and writes the output.  Every wait then
+    // points to an earlier position, which is what makes it deadlock-free.
+    S.fused_merge = opt.fused_merge;
     std::vector<int32_t> rec((size_t)L * n_heads, -1);  // leaf-head -> merge record
     std::vector<int32_t> rec_n;                          // partials per record (counting sort)
-    for (const ItemDesc& it : S.items) {
+    std::vector<int32_t> last_item;                      // fused: leaf-head -> its last item
+    if (opt.fused_merge) {
+        last_item.assign((size_t)L * n_heads, -1);
+        for (int ii = 0; ii < (int)S.items.size(); ++ii) {
+            const ItemDesc& it = S.items[ii];
+            for (int j = 0; j < it.n_slots; ++j)
+                if (S.slot_out[it.out_begin + j] != kSlotUnused)
+                    last_item[(size_t)S.slot_leaf[it.slot_begin + j] * n_heads + it.head] = ii;
+        }
+    }
+    for (int ii = 0; ii < (int)S.items.size(); ++ii) {
+        const ItemDesc& it = S.items[ii];
         for (int j = 0; j < it.n_slots; ++j) {
             int32_t& code = S.slot_out[it.out_begin + j];
             if (code == kSlotUnused) continue;
@@ -805,6 +851,10 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                 rec_n.push_back(0);
                 S.merge_leaf.push_back(leaf);
                 S.merge_head.push_back(it.head);
+            }
+            if (opt.fused_merge && last_item[key] == ii) {
+                code = kOwnerBase + rec[key];
+                continue;
             }
             code = rec[key];   // temporarily: the record
             rec_n[rec[key]]++;
@@ -821,7 +871,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     for (const ItemDesc& it : S.items)   // item order within each record
         for (int j = 0; j < it.n_slots; ++j) {
             int32_t& code = S.slot_out[it.out_begin + j];
-            if (code < 0) continue;
+            if (code < 0 || code >= kOwnerBase) continue;
             const int mi = code;
             code = fill[mi]++;
             S.part_merge[code] = mi;
@@ -831,8 +881,11 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     for (int mi = 0; mi < nrec; ++mi)
         S.merge_rec[mi] = {S.merge_leaf[mi], S.merge_head[mi], S.merge_begin[mi], rec_n[mi]};
     for (ItemDesc& it : S.items)
-        for (int j = 0; j < it.n_slots; ++j)
-            if (S.slot_out[it.out_begin + j] >= 0) it.pad |= 1;   // holds partials: takes part in merges
+        for (int j = 0; j < it.n_slots; ++j) {
+            const int32_t code = S.slot_out[it.out_begin + j];
+            if (code >= 0 && code < kOwnerBase) it.pad |= 1;   // writes partials
+            if (code >= kOwnerBase) it.pad |= 2;               // merges records (fused)
+        }
     for (int32_t l = 0; l < L; ++l)
         for (int h = 0; h < n_heads; ++h)
             if (cover[(size_t)l * n_heads + h] == 0) {

@@ -9,6 +9,9 @@
 // loaded at once -- one memory round trip after the wait.  Partials are combined in the schedule's fixed (item)
 // order, so the result does not depend on CTA timing.  The records were
 // written moments earlier and are read from L2.
+#include <mutex>
+#include <vector>
+
 #include "ta_ptx.cuh"
 
 namespace ta {
@@ -48,6 +51,28 @@ cudaError_t launch_merge(const AttnArgs& a, int n_merge, bool pdl, cudaStream_t 
     if (a.D >= 128) return cudaLaunchKernelEx(&cfg, merge_kernel<4>, a, n_merge);
     if (a.D >= 64) return cudaLaunchKernelEx(&cfg, merge_kernel<2>, a, n_merge);
     return cudaLaunchKernelEx(&cfg, merge_kernel<1>, a, n_merge);
+}
+
+}  // namespace ta
+
+namespace ta {
+
+cudaError_t set_smem_attr_once(const void* kernel, int bytes) {
+    struct Key {
+        const void* k;
+        int dev;
+    };
+    static std::mutex mu;
+    static std::vector<Key> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Key& k : done)
+        if (k.k == kernel && k.dev == dev) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.push_back({kernel, dev});
+    return e;
 }
 
 }  // namespace ta

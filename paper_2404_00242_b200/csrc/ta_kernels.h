@@ -41,6 +41,8 @@ struct AttnArgs {
     const int4* merge_rec;    // [n_merge] {leaf, local kv head, first partial id, count}
     const int32_t* part_merge;// partial id -> merge record
     int n_merge;              // merge records
+    unsigned* merge_cnt;      // fused merge: per record, partial pieces published (self-resetting)
+    int fused_merge;          // 1: owners merge in the attention launch (tcgen05 kernel)
     const int32_t* empty;     // [n_empty][2] (leaf, head)
     int n_empty;
     int n_ctas;
@@ -50,11 +52,15 @@ struct AttnArgs {
     float scale_log2;         // log2(e) / sqrt(D)
     int kv_bf16;
     int out_bf16;
-    long long* trace;         // optional clock64 trace (debug)
-    int debug;                // debug experiment bits (0 in production)
+    long long* trace;         // optional clock64 trace (debug builds of the launch: a separate instantiation)
     int prefetch_tiles;       // first tiles of each CTA prefetched into L2 before the dependency wait
     unsigned long long* timeline;   // debug: [4] = attn first start, attn last end, merge first start, merge last end (ns)
 };
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for the current device,
+// once per (kernel, device): the attribute is per device, so a process with
+// contexts on several GPUs sets it on each.
+cudaError_t set_smem_attr_once(const void* kernel, int bytes);
 
 // tcgen05/TMEM path (bf16, D = 128).
 cudaError_t launch_attn_mma(const AttnArgs& a, bool pdl, cudaStream_t s);

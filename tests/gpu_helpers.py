@@ -107,3 +107,51 @@ def run_gpu(snap, content: core.Content, d_head: int, h_q: int, h_kv: int, kv_dt
     torch.cuda.synchronize()
     o = out.float().cpu().numpy().astype(np.float64).reshape(len(leaves), -1)
     return o, (lse.cpu().numpy() if with_lse else None), ctx
+
+
+def dense_reference(snap, content: core.Content, d_head: int, h_q: int, h_kv: int, leaves, kv_heads=None):
+    """fp64 reference for full-size trees: the dense form of naive_attention
+    (attention.hpp:237-288) with the tree mask written as the ancestor relation
+    (reconstruct_dense_mask, partition.hpp:267-279): leaf l attends token t iff
+    t's node lies on l's root-to-leaf path.  One BLAS GEMM per kv head.
+    `content` holds K/V for the kv heads in `kv_heads` (default: all) side by
+    side and queries for their G q heads each.  Returns (out [L][hq*d], lse
+    [L][hq]) for the selected heads, in leaves() order."""
+    root, ids, par, cnt = snap
+    parent = {int(i): int(p) for i, p in zip(ids, par)}
+    kv_heads = list(range(h_kv)) if kv_heads is None else list(kv_heads)
+    G = h_q // h_kv
+    nodes = [int(i) for i, c in zip(ids, cnt) if int(c) > 0]
+    tok_node = np.concatenate([np.full(int(content.keys[n].shape[0]), n, np.int64) for n in nodes]) \
+        if nodes else np.zeros(0, np.int64)
+    K = np.concatenate([content.keys[n] for n in nodes]) if nodes else np.zeros((0, len(kv_heads) * d_head))
+    V = np.concatenate([content.values[n] for n in nodes]) if nodes else np.zeros((0, len(kv_heads) * d_head))
+    L = len(leaves)
+    mask = np.zeros((L, tok_node.size), bool)
+    for li, leaf in enumerate(leaves):
+        path = []
+        cur = int(leaf)
+        while cur != -1:
+            path.append(cur)
+            cur = parent[cur]
+        mask[li] = np.isin(tok_node, path)
+    Q = np.stack([content.queries[int(l)] for l in leaves]).astype(np.float64).reshape(L, len(kv_heads) * G, d_head)
+    out = np.zeros((L, len(kv_heads) * G, d_head))
+    lse = np.full((L, len(kv_heads) * G), -np.inf)
+    big = np.repeat(mask, G, axis=0)   # [L*G][N]
+    for hi in range(len(kv_heads)):
+        Kh = K[:, hi * d_head:(hi + 1) * d_head].astype(np.float64)
+        Vh = V[:, hi * d_head:(hi + 1) * d_head].astype(np.float64)
+        q = Q[:, hi * G:(hi + 1) * G, :].reshape(L * G, d_head)
+        s = (q @ Kh.T) / np.sqrt(d_head)
+        s[~big] = -np.inf
+        m = s.max(axis=1, keepdims=True)
+        ok = np.isfinite(m[:, 0])
+        m[~ok] = 0.0
+        w = np.exp(s - m)
+        den = w.sum(axis=1, keepdims=True)
+        o = (w @ Vh) / np.where(den > 0, den, 1.0)
+        out[:, hi * G:(hi + 1) * G, :] = o.reshape(L, G, d_head)
+        l_ = np.where(ok, m[:, 0] + np.log(np.where(den[:, 0] > 0, den[:, 0], 1.0)), -np.inf)
+        lse[:, hi * G:(hi + 1) * G] = l_.reshape(L, G)
+    return out.reshape(L, -1), lse

@@ -23,7 +23,7 @@ def test_library_exports_every_symbol():
     lib = ctypes.CDLL(capi.LIB_PATH)
     missing = [s for s in declared() if not hasattr(lib, s)]
     assert not missing, missing
-    assert capi.lib().ta_abi_version() == 1
+    assert capi.lib().ta_abi_version() == 2
 
 
 def test_no_oracle_linkage():

@@ -40,7 +40,7 @@ def test_golden_attention_cases():
     """Reference outputs (golden, from _ref) on the reference's own content."""
     meta, arrays = G.attention()
     for m in meta:
-        if m["d_head"] not in (16, 32, 64, 128):
+        if m["d_head"] not in (8, 16, 32, 64, 128):
             continue
         snap = G.snap(m["tree"])
         t = core.Tree.from_snapshot(snap)

@@ -13,6 +13,7 @@ from oracle import core
 from paper_2404_00242_b200 import TreeAttention
 
 UNUSED = -(1 << 31)
+OWNER = 1 << 30   # slot_out >= OWNER: the item merges record code - OWNER (fused merge)
 
 
 def _ctx(G=1, dtype="f32", n_kv=1):
@@ -82,12 +83,13 @@ def check_coverage(ctx, tree: core.Tree, bs):
                         used.add(j)
                         key = (head, slots[j], node, tok)
                         seen[key] = seen.get(key, 0) + 1
-        assert bool(flags & 1) == any(int(c) >= 0 for c in S["slot_out"][ob:ob + ns])
+        assert bool(flags & 1) == any(0 <= int(c) < OWNER for c in S["slot_out"][ob:ob + ns])
+        assert bool(flags & 2) == any(int(c) >= OWNER for c in S["slot_out"][ob:ob + ns])
         for j in range(ns):
             code = int(S["slot_out"][ob + j])
             if j in used:
                 assert code != UNUSED
-                codes.setdefault((slots[j], head), []).append(code)
+                codes.setdefault((slots[j], head), []).append((i, code))
             else:
                 assert code == UNUSED
     n_tiles = len(S["tile_ng"])
@@ -105,13 +107,21 @@ def check_coverage(ctx, tree: core.Tree, bs):
             assert all(c == 1 for c in got.values()), (li, h)
     # outputs: one direct write, or partials merged in one record
     recs = {(int(S["merge_leaf"][m]), int(S["merge_head"][m])): m for m in range(len(S["merge_leaf"]))}
-    for (li, h), cs in codes.items():
+    for (li, h), ics in codes.items():
+        cs = [c for _, c in ics]
         if len(cs) == 1:
             assert cs[0] == -1 - li and (li, h) not in recs
         else:
             m = recs[(li, h)]
             parts = [int(p) for p in S["merge_parts"][S["merge_begin"][m]:S["merge_begin"][m + 1]]]
+            if S["fused_merge"]:
+                # the leaf-head's last item owns the record; the others write partials
+                owner = [(i, c) for i, c in ics if c >= OWNER]
+                assert len(owner) == 1 and owner[0][1] == OWNER + m
+                assert owner[0][0] == max(i for i, _ in ics)
+                cs = [c for c in cs if c < OWNER]
             assert sorted(parts) == sorted(cs) and all(int(S["part_merge"][p]) == m for p in parts)
+            assert all(0 <= c < OWNER for c in cs)
     empty = {(int(l), int(h)) for l, h in S["empty"]}
     assert empty == {(li, h) for li in range(len(leaves)) for h in range(n_heads) if (li, h) not in codes}
     assert all(tree.path_tokens(leaves[li]) == 0 for li, h in empty)
@@ -126,7 +136,7 @@ def interpret(ctx, tree, content, d, h_q, h_kv, bs):
     G = h_q // h_kv
     L = len(leaves)
     out = np.zeros((L, h_q, d))
-    parts = {}
+    parts, own = {}, {}
     for i, head, tb, te, sb, ns, ob, flags in _items(S):
         slots = [int(x) for x in S["slot_leaf"][sb:sb + ns]]
         for j, li in enumerate(slots):
@@ -149,10 +159,14 @@ def interpret(ctx, tree, content, d, h_q, h_kv, bs):
             lse = (m + np.log(w.sum(1, keepdims=True))).ravel()
             if code < 0:
                 out[-1 - code] = o
+            elif code >= OWNER:
+                own[code - OWNER] = (o, lse)
             else:
                 parts[code] = (o, lse)
     for m_i, li in enumerate(S["merge_leaf"]):
         ps = [parts[int(p)] for p in S["merge_parts"][S["merge_begin"][m_i]:S["merge_begin"][m_i + 1]]]
+        if m_i in own:   # fused merge: the owner's share comes last (item order)
+            ps.append(own[m_i])
         M = np.max([p[1] for p in ps], axis=0)
         w = [np.exp(p[1] - M) for p in ps]
         out[int(li)] = sum(wi[:, None] * p[0] for wi, p in zip(w, ps)) / sum(w)[:, None]
@@ -226,6 +240,25 @@ def test_coverage_item_cost_repartition():
         t = core.random_tree(rng, max_leaves=50, max_node_tokens=200)
         ctx.restore(*t.snapshot())
         check_coverage(ctx, t, 128)
+
+
+def test_interpreter_fused_merge_matches_oracle():
+    """tcgen05 schedules (bf16, d 128) merge split leaf-heads in their last
+    item: the interpreter with owner shares reproduces naive_attention."""
+    rng = core.Rng(78)
+    for trial in range(4):
+        ctx = _ctx(G=4, dtype="bf16")
+        ctx.set_option("num_ctas", (5, 37, 148, 148)[trial])
+        t = core.random_tree(rng, max_leaves=40, max_tokens=3000, max_node_tokens=300)
+        ctx.restore(*t.snapshot())
+        S = ctx.schedule(128)
+        assert S["fused_merge"]
+        c = core.Content.synth(t, 128, trial, qdim=128 * 4)
+        got = interpret(ctx, t, c, 128, 4, 1, 128)
+        ref = core.naive_attention(t, c.expanded(128, 4, 1), 128, 4)
+        for i in range(len(ref)):
+            if t.path_tokens(int(t.leaves()[i])) > 0:
+                assert core.relative_error(got[i], ref[i]) < 1e-12
 
 
 def test_interpreter_matches_oracle():
