@@ -213,9 +213,13 @@ typedef struct ta_schedule_view {
     const int32_t* empty;       /* [n_empty][2] (leaf, local kv head) */
     int32_t n_lanes;
     int32_t use_mma;
-    int32_t fused_merge;        /* 1: slot_out codes >= 2^30 mark the item that merges record
-                                   code - 2^30 inside the attention launch (merge_parts then
-                                   lists the other items' partials only) */
+    int32_t fused_merge;        /* 1: records merged at the end of the attention launch: CTA c
+                                   publishes cta_pub[cta_pub_begin[c] ..] = (record, partials it
+                                   wrote), then merges records cta_own[cta_own_begin[c] ..] */
+    const int32_t* cta_pub_begin;  /* [n_ctas + 1] (fused_merge only, else NULL) */
+    const int32_t* cta_pub;        /* [n][2] */
+    const int32_t* cta_own_begin;  /* [n_ctas + 1] */
+    const int32_t* cta_own;        /* [n_merge] */
 } ta_schedule_view;
 ta_status ta_schedule_get(ta_ctx* ctx, int block_size, ta_schedule_view* out);
 

@@ -301,7 +301,17 @@ class TreeAttention:
                 "merge_leaf": arr(v.merge_leaf, v.n_merge), "merge_head": arr(v.merge_head, v.n_merge),
                 "merge_begin": arr(v.merge_begin, v.n_merge + 1), "merge_parts": arr(v.merge_parts, n_mp),
                 "empty": arr(v.empty, 2 * v.n_empty).reshape(-1, 2), "n_lanes": v.n_lanes,
-                "use_mma": bool(v.use_mma), "fused_merge": bool(v.fused_merge)}
+                "use_mma": bool(v.use_mma), "fused_merge": bool(v.fused_merge),
+                **self._fused_lists(v, arr)}
+
+    @staticmethod
+    def _fused_lists(v, arr):
+        if not v.fused_merge:
+            return {}
+        pb = arr(v.cta_pub_begin, v.n_ctas + 1)
+        ob = arr(v.cta_own_begin, v.n_ctas + 1)
+        return {"cta_pub_begin": pb, "cta_pub": arr(v.cta_pub, 2 * int(pb[-1])).reshape(-1, 2),
+                "cta_own_begin": ob, "cta_own": arr(v.cta_own, int(ob[-1]))}
 
     def launches_per_attend(self) -> int:
         return lib().ta_launches_per_attend(self._h)

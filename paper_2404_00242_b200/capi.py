@@ -100,7 +100,9 @@ class ScheduleView(C.Structure):
                 ("merge_head", C.POINTER(C.c_int32)), ("merge_begin", C.POINTER(C.c_int32)),
                 ("merge_parts", C.POINTER(C.c_int32)),
                 ("n_empty", C.c_int32), ("empty", C.POINTER(C.c_int32)),
-                ("n_lanes", C.c_int32), ("use_mma", C.c_int32), ("fused_merge", C.c_int32)]
+                ("n_lanes", C.c_int32), ("use_mma", C.c_int32), ("fused_merge", C.c_int32),
+                ("cta_pub_begin", C.POINTER(C.c_int32)), ("cta_pub", C.POINTER(C.c_int32)),
+                ("cta_own_begin", C.POINTER(C.c_int32)), ("cta_own", C.POINTER(C.c_int32))]
 
 
 _lib = None

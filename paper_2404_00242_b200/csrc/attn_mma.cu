@@ -19,20 +19,19 @@
 //                   the tile (sparse lanes) skip the exponentials.
 // TMEM: S0 [0,128) S1 [128,256) O [256,384) Q0 [384,448) Q1 [448,512) (Q
 // double-buffered by item parity; P aliased into the S buffer it came from).
-// At an item's end the softmax warps write each attended row as
-//   * the final output, when this item covers its leaf-head alone;
-//   * an (O/l, log2 lse) partial record, published to the leaf-head's merge
-//     counter once its bulk copy has landed (deferred by about a tile);
-//   * or, for the leaf-head's LAST item (fused merge), the merge itself: wait
-//     until the earlier items' partials are published, fold them with the
-//     on-chip share in item order, write the output.  Waits only ever point
-//     to earlier positions of the (head, lane, tile) sequence, i.e. to CTAs
-//     that are resident or done, so the grid (<= one CTA per SM) cannot
-//     deadlock.  Schedules that cannot guarantee co-residency use merge.cu.
+// At an item's end the softmax warps write each attended row either as the
+// final output (its leaf-head is covered by this item alone) or as an
+// (O/l, log2 lse) partial record, by bulk async copies.
+// Fused merge (no merge launch): at its end, once its copies have landed, a
+// CTA publishes how many partials it wrote per merge record, then merges the
+// records it owns (it wrote their last partial): it waits only for lower
+// CTAs, which publish before they merge themselves, so with every CTA
+// resident (<= one per SM) there is no wait cycle.  Otherwise merge.cu runs
+// as a second launch.
 //
 // Reference semantics: group_attention (attention.hpp:117-204) over every
-// chunk a leaf attends; tree_reduce (attention.hpp:209-233) in the owner's
-// epilogue (or merge.cu).
+// chunk a leaf attends; tree_reduce (attention.hpp:209-233) at the owner
+// CTA's end (or in merge.cu).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -120,15 +119,7 @@ __device__ __forceinline__ long long gtimer() {
         }                                                                                          \
     } while (0)
 
-// ---- fused merge: publication of partial records and the owner's wait
-// A thread's partial row-half is published once its bulk copy has completed:
-// async-proxy writes -> proxy fence -> release -> counter increment.
-__device__ __forceinline__ void publish_partial(unsigned* cnt) {
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-}
+// ---- fused merge: the owner's wait for the published partial counts
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -149,6 +140,48 @@ struct TmapSet {
     CUtensorMap k[4];   // boxes of 16, 32, 64, 128 pool rows x 64 columns
     CUtensorMap v[4];
 };
+
+// tree_reduce (attention.hpp:209-233) of 16 columns [16 chunk, +16) of one
+// merge record row (q head g): partials rec.z .. rec.z + rec.w - 1 in item
+// order, weights 2^(lse_p - max).  Loads of 4 partials in flight at a time.
+__device__ __forceinline__ void merge_chunk16(const AttnArgs& a, int4 rec, int g, int chunk) {
+    const int G = a.G;
+    float M = -INFINITY;
+    for (int p = 0; p < rec.w; ++p) M = fmaxf(M, __ldcg(a.part_lse + (size_t)(rec.z + p) * G + g));
+    float acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+    float den = 0.f;
+    for (int p0 = 0; p0 < rec.w; p0 += 4) {
+        float4 v[4][4];
+        float w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool ok = p0 + u < rec.w;
+            const size_t pid = (size_t)(rec.z + p0 + u);
+            w[u] = ok ? ex2(__ldcg(a.part_lse + pid * G + g) - M) : 0.f;
+            const float4* src = reinterpret_cast<const float4*>(a.part_o + (pid * G + g) * DH + 16 * chunk);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[u][i] = ok ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            den += w[u];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc[4 * i] = fmaf(w[u], v[u][i].x, acc[4 * i]);
+                acc[4 * i + 1] = fmaf(w[u], v[u][i].y, acc[4 * i + 1]);
+                acc[4 * i + 2] = fmaf(w[u], v[u][i].z, acc[4 * i + 2]);
+                acc[4 * i + 3] = fmaf(w[u], v[u][i].w, acc[4 * i + 3]);
+            }
+        }
+    }
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    const size_t ob = ((size_t)rec.x * a.hq_loc + (size_t)rec.y * G + g) * DH + 16 * chunk;
+    store_row<16>(a.out, ob, acc, inv, a.out_bf16);
+    if (chunk == 0 && a.lse)
+        a.lse[(size_t)rec.x * a.hq_loc + (size_t)rec.y * G + g] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
+}
 
 template <bool TRACE>
 __global__ void __launch_bounds__(NTHREADS, 1)
@@ -418,7 +451,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             q_store(qv, 0);
         }
         int gt = 0;
-        int pend = -1;   // merge record of this thread's last partial, not yet published (fused merge)
         for (int k = 0; k < n_items; ++k) {
             const ItemDesc I = item_at(k);
             const int nrows = I.n_slots * G;
@@ -550,11 +582,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     tc_fence_after();
                     q_store(qv, (k + 1) & 1);
                 }
-                if (pend >= 0 && t == I.tile_begin + 1) {
-                    // the previous item's partial has had a tile to land: publish it
-                    publish_partial(a.merge_cnt + pend);
-                    pend = -1;
-                }
             }
 
             // ---- epilogue
@@ -566,51 +593,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             named_bar(1 + q4, 64);
             l += redl[(h ^ 1) * BM + r];
             TA_TRACE_EPI(a, k, 4);
-            // an unpublished partial of the previous item goes out before this
-            // item may wait on anyone (deadlock freedom of the fused merge)
-            if (pend >= 0) {
-                publish_partial(a.merge_cnt + pend);
-                pend = -1;
-            }
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            float lse2 = m + log2f(l);
-            // fused merge (owner rows): fold the earlier items' partials in item
-            // order, then this item's share; weights relative to the common max
-            const bool owner = code >= kOwnerBase;
-            int4 rec = make_int4(0, 0, 0, 0);
-            float s_own = inv;
-            if (owner) {
-                rec = __ldg(a.merge_rec + (code - kOwnerBase));
-                wait_pieces(a.merge_cnt + (code - kOwnerBase), (unsigned)(rec.w * 2 * G));
-                float M = lse2;
-                for (int p = 0; p < rec.w; ++p) M = fmaxf(M, __ldcg(a.part_lse + (size_t)(rec.z + p) * G + g_in));
-                float den = ex2(lse2 - M);
-                for (int p = 0; p < rec.w; ++p) den += ex2(__ldcg(a.part_lse + (size_t)(rec.z + p) * G + g_in) - M);
-                s_own = ex2(lse2 - M) * inv / den;
-                lse2 = M + log2f(den);
-            }
+            const float lse2 = m + log2f(l);
             if (code != kSlotUnused && h == 0) {
-                if (code < 0 || owner) {
-                    const int leaf = owner ? rec.x : -1 - code;
-                    if (a.lse) a.lse[(size_t)leaf * a.hq_loc + I.head * G + g_in] = lse2 * kLn2;
+                if (code < 0) {
+                    if (a.lse) a.lse[(size_t)(-1 - code) * a.hq_loc + I.head * G + g_in] = lse2 * kLn2;
                 } else {
                     a.part_lse[(size_t)code * G + g_in] = lse2;
                 }
             }
             if (warp_live) {
-                // O (scaled) -> this thread's staging row (its TMEM lane = output
-                // row, its 64 columns), then one bulk async copy of the row to the
+                // O / l -> this thread's staging row (its TMEM lane = output row,
+                // its 64 columns), then one bulk async copy of the row to the
                 // final output or the partial record: the stores drain in the
                 // background instead of stalling the softmax warps behind the
                 // saturated read stream.  Compact loops: this code runs once per
                 // item, I-cache cold.
                 const uint32_t srow = sbase + SMEM_EPI + (uint32_t)(((warp - SOFT0) * 32 + lane) * EPI_ROW);
-                const bool out_final = code < 0 || owner;
-                const bool st_bf16 = out_final && a.out_bf16;
+                const bool st_bf16 = code < 0 && a.out_bf16;
                 // the row's previous bulk copy (an earlier item) has read the staging
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 TA_TRACE_EPI(a, k, 3);
-                const bool stage_f32 = !st_bf16 || owner;   // owners accumulate in fp32 first
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     uint32_t o[16];
@@ -621,8 +624,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     float f[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(o[i]) * s_own;
-                    if (!stage_f32) {
+                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(o[i]) * inv;
+                    if (st_bf16) {
                         sts128(srow + (uint32_t)(c * 32), pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]),
                                pack_bf16(f[6], f[7]));
                         sts128(srow + (uint32_t)(c * 32 + 16), pack_bf16(f[8], f[9]), pack_bf16(f[10], f[11]),
@@ -634,56 +637,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                    __float_as_uint(f[4 * q + 2]), __float_as_uint(f[4 * q + 3]));
                     }
                 }
-                if (owner) {
-                    const float M = lse2;   // final lse: w_p / den = 2^(lse_p - lse)
-#pragma unroll 1
-                    for (int p = 0; p < rec.w; ++p) {
-                        const size_t pid = (size_t)(rec.z + p);
-                        const float w = ex2(__ldcg(a.part_lse + pid * G + g_in) - M);
-                        const float4* src = reinterpret_cast<const float4*>(a.part_o + (pid * G + g_in) * DH + 64 * h);
-#pragma unroll 1
-                        for (int hh = 0; hh < 16; hh += 8) {
-                        float4 v[8];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) v[i] = __ldcg(src + hh + i);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const uint32_t sa = srow + 16u * (hh + i);
-                            float4 x = lds128f(sa);
-                            x.x = fmaf(w, v[i].x, x.x);
-                            x.y = fmaf(w, v[i].y, x.y);
-                            x.z = fmaf(w, v[i].z, x.z);
-                            x.w = fmaf(w, v[i].w, x.w);
-                            sts128(sa, __float_as_uint(x.x), __float_as_uint(x.y), __float_as_uint(x.z), __float_as_uint(x.w));
-                        }
-                        }
-                    }
-                    if (st_bf16) {   // fp32 staging -> bf16 in place (first 128 bytes, front to back)
-#pragma unroll 1
-                        for (int i = 0; i < 8; ++i) {
-                            const float4 x0 = lds128f(srow + 32u * i), x1 = lds128f(srow + 32u * i + 16u);
-                            sts128(srow + 16u * i, pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y),
-                                   pack_bf16(x1.z, x1.w));
-                        }
-                    }
-                    // the record's counter is ours alone now: the last of its 2G
-                    // readers resets it for the next launch
-                    const unsigned target = (unsigned)(rec.w * 2 * G);
-                    if (atomicAdd(a.merge_cnt + (code - kOwnerBase), 1u) == target + 2u * G - 1u)
-                        a.merge_cnt[code - kOwnerBase] = 0u;
-                }
                 if (code != kSlotUnused) {
-                    const int leaf = owner ? rec.x : -1 - code;
-                    void* dst = !out_final ? static_cast<void*>(a.part_o + ((size_t)code * G + g_in) * DH + 64 * h)
-                                           : static_cast<void*>(reinterpret_cast<char*>(a.out) +
-                                                                (((size_t)leaf * a.hq_loc + I.head * G + g_in) * DH + 64 * h) *
-                                                                    (a.out_bf16 ? 2 : 4));
+                    void* dst = code >= 0 ? static_cast<void*>(a.part_o + ((size_t)code * G + g_in) * DH + 64 * h)
+                                          : static_cast<void*>(reinterpret_cast<char*>(a.out) +
+                                                               (((size_t)(-1 - code) * a.hq_loc + I.head * G + g_in) * DH + 64 * h) *
+                                                                   (a.out_bf16 ? 2 : 4));
                     fence_proxy_async();   // the staging writes -> visible to the bulk copy
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(srow),
                                  "r"(st_bf16 ? 128u : 256u)
                                  : "memory");
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                    if (!out_final && a.fused_merge) pend = __ldg(a.part_merge + code);
                 }
             }
             TA_TRACE_EPI(a, k, 2);
@@ -693,13 +656,48 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (a.trace && lane == 0) a.trace[blockIdx.x * TRACE_SLOTS + 224 + warp - SOFT0] = clock64();
             }
         }
-        if (pend >= 0) publish_partial(a.merge_cnt + pend);
     }
 
     // the epilogues' bulk copies are complete (writes performed) before exit
-    if (warp >= SOFT0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // or, with the fused merge, before this CTA's partials are published
+    if (warp >= SOFT0) {
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if (a.fused_merge) asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     tc_fence_before();
     __syncthreads();
+    if (TRACE && a.trace && threadIdx.x == 0) a.trace[blockIdx.x * TRACE_SLOTS + 6] = gtimer();   // items done, copies landed
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+    if (a.fused_merge) {
+        // 1. publish: per record this CTA wrote partials for, one release-add
+        //    of their count
+        const int p0 = a.cta_pub_begin[blockIdx.x], p1 = a.cta_pub_begin[blockIdx.x + 1];
+        for (int i = p0 + (int)threadIdx.x; i < p1; i += NTHREADS) {
+            const int2 pb = a.cta_pub[i];
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(a.merge_cnt + pb.x), "r"(pb.y) : "memory");
+        }
+        // 2. merge the records this CTA owns, all threads: one thread per
+        //    (record, q head, 16-column chunk), tree_reduce in item order.
+        //    Every CTA has published before it waits here, so no wait can
+        //    block a publication.
+        const int o0 = a.cta_own_begin[blockIdx.x], o1 = a.cta_own_begin[blockIdx.x + 1];
+        const int G = a.G;
+        for (int u = threadIdx.x; u < (o1 - o0) * G * 8; u += NTHREADS) {
+            const int mi = a.cta_own[o0 + u / (G * 8)];
+            const int g = (u / 8) % G, chunk = u % 8;
+            const int4 rec = __ldg(a.merge_rec + mi);
+            wait_pieces(a.merge_cnt + mi, (unsigned)rec.w);
+            merge_chunk16(a, rec, g, chunk);
+        }
+        __syncthreads();
+        // the counters are ours alone now: reset them for the next launch
+        // (which publishes only after its dependency wait, i.e. after this grid)
+        for (int i = o0 + (int)threadIdx.x; i < o1; i += NTHREADS) a.merge_cnt[a.cta_own[i]] = 0u;
+    }
     if (TRACE && threadIdx.x == 0) timeline_mark(a.timeline, 0, false);
     if (TRACE && a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS + 1] = gtimer();
@@ -707,10 +705,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int nt = 0;
         for (int k = 0; k < n_items; ++k) nt += item_at(k).tile_end - item_at(k).tile_begin;
         a.trace[blockIdx.x * TRACE_SLOTS + 3] = nt;
-    }
-    if (warp == 1) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
     }
 }
 

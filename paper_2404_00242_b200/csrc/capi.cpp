@@ -62,6 +62,10 @@ struct ta_ctx {
     const int4* d_merge_rec = nullptr;
     const int32_t* d_part_merge = nullptr;
     const int32_t* d_empty = nullptr;
+    const int32_t* d_cta_pub_begin = nullptr;
+    const int2* d_cta_pub = nullptr;
+    const int32_t* d_cta_own_begin = nullptr;
+    const int32_t* d_cta_own = nullptr;
     unsigned* merge_cnt = nullptr;   // fused merge counters, one per merge record
     size_t merge_cnt_cap = 0;        // bytes
     bool fused_merge = true;         // option "fused_merge"
@@ -541,7 +545,7 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             size_t bytes;
             size_t off;
         };
-        Part parts[13] = {
+        Part parts[15] = {
             {S.tiles.data(), S.tiles.size() * sizeof(TileDesc), 0},
             {S.tile_meta.data(), S.tile_meta.size() * sizeof(TileMeta), 0},
             {S.grp_row.data(), S.grp_row.size() * 4, 0},
@@ -552,9 +556,11 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             {S.slot_out.data(), S.slot_out.size() * 4, 0},
             {S.merge_rec.data(), S.merge_rec.size() * 16, 0},
             {S.part_merge.data(), S.part_merge.size() * 4, 0},
-            {nullptr, 0, 0},
-            {nullptr, 0, 0},
+            {S.cta_pub_begin.data(), S.cta_pub_begin.size() * 4, 0},
+            {S.cta_pub.data(), S.cta_pub.size() * 8, 0},
             {S.empty.data(), S.empty.size() * 4, 0},
+            {S.cta_own_begin.data(), S.cta_own_begin.size() * 4, 0},
+            {S.cta_own.data(), S.cta_own.size() * 4, 0},
         };
         size_t total = 0;
         for (auto& p : parts) {
@@ -583,6 +589,10 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         c->d_merge_rec = (const int4*)(d + parts[8].off);
         c->d_part_merge = (const int32_t*)(d + parts[9].off);
         c->d_empty = (const int32_t*)(d + parts[12].off);
+        c->d_cta_pub_begin = (const int32_t*)(d + parts[10].off);
+        c->d_cta_pub = (const int2*)(d + parts[11].off);
+        c->d_cta_own_begin = (const int32_t*)(d + parts[13].off);
+        c->d_cta_own = (const int32_t*)(d + parts[14].off);
         // fused-merge counters: zero at every prepare (self-resetting in the kernel)
         const size_t cb = sizeof(unsigned) * std::max<size_t>(1, S.merge_rec.size());
         if (cb > c->merge_cnt_cap) {
@@ -638,6 +648,10 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.n_merge = (int)S.merge_rec.size();
     a.merge_cnt = c->merge_cnt;
     a.fused_merge = S.fused_merge ? 1 : 0;
+    a.cta_pub_begin = c->d_cta_pub_begin;
+    a.cta_pub = c->d_cta_pub;
+    a.cta_own_begin = c->d_cta_own_begin;
+    a.cta_own = c->d_cta_own;
     a.empty = c->d_empty;
     a.n_empty = (int)(S.empty.size() / 2);
     a.n_ctas = (int)S.cta_begin.size() - 1;
@@ -759,7 +773,9 @@ ta_status ta_io_stats_get(ta_ctx* c, ta_io_stats* o) {
         o->meta_bytes = (int64_t)(S.tiles.size() * (sizeof(TileDesc) + sizeof(TileMeta)) +
                                   S.items.size() * sizeof(ItemDesc)) +
                         (int64_t)(S.grp_row.size() + S.grp_info.size() + S.cta_begin.size() + S.slot_leaf.size() +
-                                  S.slot_out.size() + 4 * S.merge_rec.size() + S.empty.size()) * 4;
+                                  S.slot_out.size() + 4 * S.merge_rec.size() + S.part_merge.size() + S.empty.size() +
+                                  S.cta_pub_begin.size() + 2 * S.cta_pub.size() + S.cta_own_begin.size() +
+                                  S.cta_own.size()) * 4;
         o->flops = S.masked_q_tokens * c->hq_loc * 4 * D;
     });
 }
@@ -796,6 +812,12 @@ ta_status ta_schedule_get(ta_ctx* c, int bs, ta_schedule_view* o) {
         o->n_lanes = S.n_lanes;
         o->use_mma = effective_opts(c).use_mma ? 1 : 0;
         o->fused_merge = S.fused_merge ? 1 : 0;
+        if (S.fused_merge) {
+            o->cta_pub_begin = S.cta_pub_begin.data();
+            o->cta_pub = reinterpret_cast<const int32_t*>(S.cta_pub.data());
+            o->cta_own_begin = S.cta_own_begin.data();
+            o->cta_own = S.cta_own.data();
+        }
     });
 }
 

@@ -459,8 +459,8 @@ std::string plan_json(const Tree& t, const Plan& p) {
 //    run's maximal (head, lane) pieces are its items.
 // 4. Outputs.  A leaf-head attended by one item is written directly; else
 //    its items write partials that are merged in item order (tree_reduce,
-//    attention.hpp:209-233): by the leaf-head's last item inside the attention
-//    launch (fused merge, tcgen05 kernel) or by the merge launch after it.
+//    attention.hpp:209-233): at the end of the attention launch by the highest
+//    CTA that wrote one of them (fused merge) or by the merge launch after it.
 // ===========================================================================
 namespace {
 
@@ -818,25 +818,10 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     }
     // Partial ids are contiguous per merge record (record mi owns ids
     // [merge_begin[mi], merge_begin[mi+1]) in item order), so a merge reads
-    // them without an id list.  Fused merge: the record's LAST item (largest
-    // position in the (head, lane, tile) sequence) keeps its share on chip,
-    // waits for the others' partials and writes the output.  Every wait then
-    // points to an earlier position, which is what makes it deadlock-free.
-    S.fused_merge = opt.fused_merge;
+    // them without an id list.
     std::vector<int32_t> rec((size_t)L * n_heads, -1);  // leaf-head -> merge record
     std::vector<int32_t> rec_n;                          // partials per record (counting sort)
-    std::vector<int32_t> last_item;                      // fused: leaf-head -> its last item
-    if (opt.fused_merge) {
-        last_item.assign((size_t)L * n_heads, -1);
-        for (int ii = 0; ii < (int)S.items.size(); ++ii) {
-            const ItemDesc& it = S.items[ii];
-            for (int j = 0; j < it.n_slots; ++j)
-                if (S.slot_out[it.out_begin + j] != kSlotUnused)
-                    last_item[(size_t)S.slot_leaf[it.slot_begin + j] * n_heads + it.head] = ii;
-        }
-    }
-    for (int ii = 0; ii < (int)S.items.size(); ++ii) {
-        const ItemDesc& it = S.items[ii];
+    for (const ItemDesc& it : S.items) {
         for (int j = 0; j < it.n_slots; ++j) {
             int32_t& code = S.slot_out[it.out_begin + j];
             if (code == kSlotUnused) continue;
@@ -851,10 +836,6 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                 rec_n.push_back(0);
                 S.merge_leaf.push_back(leaf);
                 S.merge_head.push_back(it.head);
-            }
-            if (opt.fused_merge && last_item[key] == ii) {
-                code = kOwnerBase + rec[key];
-                continue;
             }
             code = rec[key];   // temporarily: the record
             rec_n[rec[key]]++;
@@ -871,7 +852,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     for (const ItemDesc& it : S.items)   // item order within each record
         for (int j = 0; j < it.n_slots; ++j) {
             int32_t& code = S.slot_out[it.out_begin + j];
-            if (code < 0 || code >= kOwnerBase) continue;
+            if (code < 0) continue;
             const int mi = code;
             code = fill[mi]++;
             S.part_merge[code] = mi;
@@ -881,11 +862,57 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     for (int mi = 0; mi < nrec; ++mi)
         S.merge_rec[mi] = {S.merge_leaf[mi], S.merge_head[mi], S.merge_begin[mi], rec_n[mi]};
     for (ItemDesc& it : S.items)
-        for (int j = 0; j < it.n_slots; ++j) {
-            const int32_t code = S.slot_out[it.out_begin + j];
-            if (code >= 0 && code < kOwnerBase) it.pad |= 1;   // writes partials
-            if (code >= kOwnerBase) it.pad |= 2;               // merges records (fused)
+        for (int j = 0; j < it.n_slots; ++j)
+            if (S.slot_out[it.out_begin + j] >= 0) it.pad |= 1;   // holds partials: takes part in merges
+
+    // Fused merge (tcgen05 kernel): no merge launch.  At its end, after all
+    // its items, a CTA publishes the partials it wrote (per record: how many)
+    // and only then merges the records it owns.  Publication never waits, so
+    // no CTA's wait can block another's: any ownership is deadlock-free while
+    // every CTA is resident (<= one per SM).  Records are spread evenly over
+    // the CTAs by merge work (rows x partials).
+    S.fused_merge = opt.fused_merge;
+    if (opt.fused_merge) {
+        const int n_cta = (int)S.cta_begin.size() - 1;
+        std::vector<int32_t> owner(nrec, -1);
+        S.cta_pub_begin.assign(1, 0);
+        std::vector<int32_t> cnt_here(nrec, 0), touched_recs;
+        for (int c = 0; c < n_cta; ++c) {
+            touched_recs.clear();
+            for (int ii = S.cta_begin[c]; ii < S.cta_begin[c + 1]; ++ii) {
+                const ItemDesc& it = S.items[ii];
+                for (int j = 0; j < it.n_slots; ++j) {
+                    const int32_t code = S.slot_out[it.out_begin + j];
+                    if (code < 0) continue;
+                    const int mi = S.part_merge[code];
+                    if (cnt_here[mi]++ == 0) touched_recs.push_back(mi);
+                }
+            }
+            for (int mi : touched_recs) {
+                S.cta_pub.push_back({mi, cnt_here[mi]});
+                cnt_here[mi] = 0;
+            }
+            S.cta_pub_begin.push_back((int32_t)S.cta_pub.size());
         }
+        // even split of the records' merge work (G rows x (1 + partials) each)
+        // into contiguous record ranges, one per CTA
+        {
+            int64_t total = 0;
+            for (int mi = 0; mi < nrec; ++mi) total += 1 + rec_n[mi];
+            int64_t acc = 0;
+            for (int mi = 0; mi < nrec; ++mi) {
+                owner[mi] = (int)std::min<int64_t>(n_cta - 1, (acc * n_cta) / std::max<int64_t>(1, total));
+                acc += 1 + rec_n[mi];
+            }
+        }
+        std::vector<int32_t> own_n(n_cta + 1, 0);
+        for (int mi = 0; mi < nrec; ++mi) own_n[owner[mi] + 1]++;
+        S.cta_own_begin.assign(n_cta + 1, 0);
+        for (int c = 0; c < n_cta; ++c) S.cta_own_begin[c + 1] = S.cta_own_begin[c] + own_n[c + 1];
+        S.cta_own.resize(nrec);
+        std::vector<int32_t> pos(S.cta_own_begin.begin(), S.cta_own_begin.end() - 1);
+        for (int mi = 0; mi < nrec; ++mi) S.cta_own[pos[owner[mi]]++] = mi;
+    }
     for (int32_t l = 0; l < L; ++l)
         for (int h = 0; h < n_heads; ++h)
             if (cover[(size_t)l * n_heads + h] == 0) {

@@ -138,8 +138,9 @@ std::string plan_json(const Tree& t, const Plan& p);           // serde.hpp:41-6
 //           the (head, lane, tile) sequence balanced by cost
 // Items whose leaf-head is covered by one item write the final output
 // directly.  Otherwise the leaf-head's items write (O/l, log2 lse) partial
-// records, merged in item order (deterministic): by its last item, which
-// keeps its own share on chip (fused merge), or by the merge launch.
+// records, merged in item order (deterministic): at the end of the attention
+// launch by the highest CTA that wrote one of them (fused merge), or by the
+// merge launch.
 struct TileDesc {          // 16 bytes, read by the device
     int32_t grp_begin;     // into grp_row / grp_info
     uint8_t ng;            // groups in the tile (1..8)
@@ -169,7 +170,6 @@ struct ItemDesc {          // 32 bytes, read by the device
 static_assert(sizeof(ItemDesc) == 32, "ItemDesc layout");
 
 constexpr int32_t kSlotUnused = INT32_MIN;   // slot_out: slot not attended in this item
-constexpr int32_t kOwnerBase = 1 << 30;      // slot_out >= kOwnerBase: the item owns merge record code - kOwnerBase
 
 inline uint32_t grp_pack(int count, int b, int e) {
     return (uint32_t)count | ((uint32_t)b << 8) | ((uint32_t)e << 20);
@@ -183,8 +183,7 @@ struct Schedule {
     std::vector<ItemDesc> items;
     std::vector<int32_t> cta_begin;   // [n_ctas + 1] into items
     std::vector<int32_t> slot_leaf;   // lanes' slots: leaf index (leaves() order)
-    std::vector<int32_t> slot_out;    // per item slot: -1 - leaf (direct), partial id, kOwnerBase + merge
-                                      // record (fused merge: the record's last item merges it), or kSlotUnused
+    std::vector<int32_t> slot_out;    // per item slot: -1 - leaf (direct), partial id, or kSlotUnused
     std::vector<int32_t> part_merge;  // partial id -> merge record
     std::vector<int32_t> merge_leaf, merge_head;  // merge record -> leaf index, local kv head
     std::vector<int32_t> merge_begin; // [n_merge + 1] into merge_parts
@@ -192,9 +191,17 @@ struct Schedule {
     struct MergeRec {
         int32_t leaf, head, pbegin, n;
     };
-    std::vector<MergeRec> merge_rec;  // device copy: one 16-byte load per record (n = partials written; with
-                                      // the fused merge the owner item's own share is not among them)
+    std::vector<MergeRec> merge_rec;  // device copy: one 16-byte load per record
+    // fused merge (tcgen05 kernel): per CTA, the records it wrote partials for
+    // (record, partial count) and the records it merges at its end
     bool fused_merge = false;
+    struct Pub {
+        int32_t rec, n;
+    };
+    std::vector<int32_t> cta_pub_begin;   // [n_ctas + 1] into cta_pub
+    std::vector<Pub> cta_pub;
+    std::vector<int32_t> cta_own_begin;   // [n_ctas + 1] into cta_own
+    std::vector<int32_t> cta_own;         // merge records
     std::vector<int32_t> empty;       // [n][2] (leaf, local head) pairs with no path tokens
     int32_t n_lanes = 0;
     int32_t max_lane_rows = 0;        // max rows (slots x G) of any lane
@@ -210,6 +217,7 @@ struct Schedule {
         slot_leaf.clear(); slot_out.clear(); part_merge.clear(); merge_leaf.clear(); merge_head.clear();
         merge_begin.clear(); merge_parts.clear(); merge_rec.clear(); empty.clear();
         fused_merge = false;
+        cta_pub_begin.clear(); cta_pub.clear(); cta_own_begin.clear(); cta_own.clear();
         n_lanes = n_partials = n_leaves = max_lane_rows = 0;
         kv_tokens_unique = kv_rows_loaded = masked_q_tokens = n_stripes = 0;
     }
@@ -230,8 +238,9 @@ struct SchedOptions {
     bool use_mma = true;       // bf16 d128 only
     int fma_max_rows = 8;      // rows per lane of the FMA kernel (8 or 16)
     bool final_direct = true;  // single-item leaf-heads written directly
-    bool fused_merge = false;  // split leaf-heads merged inside the attention launch by their last item
-                               // (tcgen05 kernel, all CTAs co-resident); else by the merge launch
+    bool fused_merge = false;  // split leaf-heads merged inside the attention launch, at the end of the
+                               // highest CTA that wrote one of their partials (tcgen05 kernel, all CTAs
+                               // co-resident); else by the merge launch
     int64_t trace_ptr = 0;     // debug: device buffer for the kernel's clock64 trace
 };
 

@@ -41,8 +41,12 @@ struct AttnArgs {
     const int4* merge_rec;    // [n_merge] {leaf, local kv head, first partial id, count}
     const int32_t* part_merge;// partial id -> merge record
     int n_merge;              // merge records
-    unsigned* merge_cnt;      // fused merge: per record, partial pieces published (self-resetting)
-    int fused_merge;          // 1: owners merge in the attention launch (tcgen05 kernel)
+    unsigned* merge_cnt;      // fused merge: per record, partials published (self-resetting)
+    int fused_merge;          // 1: records merged at the end of the attention launch (tcgen05 kernel)
+    const int32_t* cta_pub_begin;   // [n_ctas + 1] into cta_pub
+    const int2* cta_pub;            // (record, partials this CTA wrote)
+    const int32_t* cta_own_begin;   // [n_ctas + 1] into cta_own
+    const int32_t* cta_own;         // records the CTA merges
     const int32_t* empty;     // [n_empty][2] (leaf, head)
     int n_empty;
     int n_ctas;

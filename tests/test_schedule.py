@@ -13,7 +13,6 @@ from oracle import core
 from paper_2404_00242_b200 import TreeAttention
 
 UNUSED = -(1 << 31)
-OWNER = 1 << 30   # slot_out >= OWNER: the item merges record code - OWNER (fused merge)
 
 
 def _ctx(G=1, dtype="f32", n_kv=1):
@@ -83,8 +82,7 @@ def check_coverage(ctx, tree: core.Tree, bs):
                         used.add(j)
                         key = (head, slots[j], node, tok)
                         seen[key] = seen.get(key, 0) + 1
-        assert bool(flags & 1) == any(0 <= int(c) < OWNER for c in S["slot_out"][ob:ob + ns])
-        assert bool(flags & 2) == any(int(c) >= OWNER for c in S["slot_out"][ob:ob + ns])
+        assert bool(flags & 1) == any(int(c) >= 0 for c in S["slot_out"][ob:ob + ns])
         for j in range(ns):
             code = int(S["slot_out"][ob + j])
             if j in used:
@@ -107,6 +105,15 @@ def check_coverage(ctx, tree: core.Tree, bs):
             assert all(c == 1 for c in got.values()), (li, h)
     # outputs: one direct write, or partials merged in one record
     recs = {(int(S["merge_leaf"][m]), int(S["merge_head"][m])): m for m in range(len(S["merge_leaf"]))}
+    own, pub = {}, {}
+    if S["fused_merge"]:
+        for c in range(len(cb) - 1):
+            for m in S["cta_own"][S["cta_own_begin"][c]:S["cta_own_begin"][c + 1]]:
+                assert int(m) not in own
+                own[int(m)] = c
+            for m, n in S["cta_pub"][S["cta_pub_begin"][c]:S["cta_pub_begin"][c + 1]]:
+                pub[(c, int(m))] = int(n)
+        assert set(own) == set(range(len(S["merge_leaf"])))
     for (li, h), ics in codes.items():
         cs = [c for _, c in ics]
         if len(cs) == 1:
@@ -114,14 +121,13 @@ def check_coverage(ctx, tree: core.Tree, bs):
         else:
             m = recs[(li, h)]
             parts = [int(p) for p in S["merge_parts"][S["merge_begin"][m]:S["merge_begin"][m + 1]]]
-            if S["fused_merge"]:
-                # the leaf-head's last item owns the record; the others write partials
-                owner = [(i, c) for i, c in ics if c >= OWNER]
-                assert len(owner) == 1 and owner[0][1] == OWNER + m
-                assert owner[0][0] == max(i for i, _ in ics)
-                cs = [c for c in cs if c < OWNER]
             assert sorted(parts) == sorted(cs) and all(int(S["part_merge"][p]) == m for p in parts)
-            assert all(0 <= c < OWNER for c in cs)
+            if S["fused_merge"]:
+                # every CTA that wrote one of its partials publishes their count
+                cta_of = np.searchsorted(cb, [i for i, _ in ics], side="right") - 1
+                assert m in own
+                for c in set(cta_of):
+                    assert pub[(c, m)] == sum(1 for x in cta_of if x == c)
     empty = {(int(l), int(h)) for l, h in S["empty"]}
     assert empty == {(li, h) for li in range(len(leaves)) for h in range(n_heads) if (li, h) not in codes}
     assert all(tree.path_tokens(leaves[li]) == 0 for li, h in empty)
@@ -136,7 +142,7 @@ def interpret(ctx, tree, content, d, h_q, h_kv, bs):
     G = h_q // h_kv
     L = len(leaves)
     out = np.zeros((L, h_q, d))
-    parts, own = {}, {}
+    parts = {}
     for i, head, tb, te, sb, ns, ob, flags in _items(S):
         slots = [int(x) for x in S["slot_leaf"][sb:sb + ns]]
         for j, li in enumerate(slots):
@@ -159,14 +165,10 @@ def interpret(ctx, tree, content, d, h_q, h_kv, bs):
             lse = (m + np.log(w.sum(1, keepdims=True))).ravel()
             if code < 0:
                 out[-1 - code] = o
-            elif code >= OWNER:
-                own[code - OWNER] = (o, lse)
             else:
                 parts[code] = (o, lse)
     for m_i, li in enumerate(S["merge_leaf"]):
         ps = [parts[int(p)] for p in S["merge_parts"][S["merge_begin"][m_i]:S["merge_begin"][m_i + 1]]]
-        if m_i in own:   # fused merge: the owner's share comes last (item order)
-            ps.append(own[m_i])
         M = np.max([p[1] for p in ps], axis=0)
         w = [np.exp(p[1] - M) for p in ps]
         out[int(li)] = sum(wi[:, None] * p[0] for wi, p in zip(w, ps)) / sum(w)[:, None]
