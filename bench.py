@@ -10,6 +10,11 @@ layer (n_layers x ta_attend), inputs resident in HBM.  Each layer has its own
 KV pool, so the per-step working set (3.1 GB for config B) is far larger than
 L2 and nothing is served from L2 across layers or steps.
 
+The headline line is config B (few-shot, BASELINE.json configs[1]).  At N = 1
+the default run also measures the other benchmarked configs (C reasoning, D
+speculative t64 / t256, E's per-GPU shard) and reports them under "configs"
+with their own roofline, e2e and CPU baseline (--headline-only skips them).
+
 Multi-GPU (torchrun): kv heads are sharded across ranks (head sharding, no
 collective on the attention path); every rank runs the whole tree for its
 heads, `value` is the whole-job step latency = max over ranks.
@@ -21,8 +26,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -45,10 +50,14 @@ CONFIGS = {
     # configs[3]: speculative token trees
     "spec_t64": dict(kind="spec", prompt=4000, tree_size=64, n_layers=32, h_q=32, h_kv=8, d=128, dtype="bf16"),
     "spec_t256": dict(kind="spec", prompt=16000, tree_size=256, n_layers=32, h_q=32, h_kv=8, d=128, dtype="bf16"),
-    # configs[4]: Llama-3-70B shapes, 32k prefix few-shot
+    # configs[4]: Llama-3-70B shapes, 32k prefix few-shot: all 8 kv heads on one GPU ...
     "few_shot_70b": dict(kind="few_shot", prefix=32000, branches=50, iteration=400, n_layers=80, h_q=64, h_kv=8,
                          d=128, dtype="bf16"),
+    # ... and the per-GPU shard of the 8-GPU head-sharded run (1 kv head + its 8 q heads)
+    "few_shot_70b_shard": dict(kind="few_shot", prefix=32000, branches=50, iteration=400, n_layers=80, h_q=64,
+                               h_kv=8, n_local_kv_heads=1, d=128, dtype="bf16"),
 }
+SUB_CONFIGS = ["reasoning", "spec_t64", "spec_t256", "few_shot_70b_shard"]
 
 
 # ------------------------------------------------------------------ trees
@@ -103,66 +112,66 @@ def spec_tree(prompt, t_size):
     return holder_token_tree(prompt, t_size)
 
 
+def local_kv_heads(cfg, world):
+    return cfg.get("n_local_kv_heads") or cfg["h_kv"] // world
+
+
 # ------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 50 ms in the
-    background; summary() keeps the samples inside [mark_start, mark_end]."""
+    """SM clocks and throttle reasons polled through NVML every `period`
+    seconds in a background thread; summary() keeps the samples taken inside
+    [mark_start, mark_end] (the timed region)."""
 
-    def __init__(self, gpu_index=0):
-        self.gpu = gpu_index
+    NAMES = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+
+    def __init__(self, gpu_index=0, period=0.002):
+        self.gpu, self.period = gpu_index, period
         self.samples = []
-        self._p = None
         self.t0 = self.t1 = None
+        self._stop = threading.Event()
+        self._th = None
+        self.max_mhz = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                        "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
-            self._t.start()
-        except FileNotFoundError:
-            self._p = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((time.perf_counter(), sm, rs))
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+            self._th = threading.Thread(target=run, daemon=True)
+            self._th.start()
+        except Exception:
+            self._th = None
         return self
 
-    def _read(self):
-        for line in self._p.stdout:
-            self.samples.append((time.time(), [x.strip() for x in line.split(",")]))
-
     def mark_start(self):
-        self.t0 = time.time()
+        self.t0 = time.perf_counter()
 
     def mark_end(self):
-        self.t1 = time.time()
+        self.t1 = time.perf_counter()
 
     def __exit__(self, *a):
-        if self._p:
-            self._p.terminate()
-            try:
-                self._p.wait(timeout=2)
-            except subprocess.TimeoutExpired:
-                self._p.kill()
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=1)
 
     def summary(self):
-        smp = self.samples
-        if self.t0 is not None and self.t1 is not None:
-            inside = [x for x in smp if self.t0 <= x[0] <= self.t1]
-            smp = inside or sorted(smp, key=lambda x: abs(x[0] - (self.t0 + self.t1) / 2))[:1]
-        smp = [x[1] for x in smp]
+        smp = [s for s in self.samples if self.t0 is not None and self.t0 <= s[0] <= (self.t1 or 1e30)]
         if not smp:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in smp if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in smp if len(s) > 1 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in smp:
-            for n, v in zip(names, s[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(smp)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        reasons = sorted(n for n, bit in self.NAMES.items() if any(s[2] & bit for s in smp))
+        return {"sm_mhz": statistics.median(s[1] for s in smp), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(smp), "source": "NVML, polled every 2 ms inside the timed region"}
 
 
 def measured_peaks():
@@ -195,99 +204,82 @@ def profile_traffic(config_name):
         return None
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
 # ------------------------------------------------------------- CPU baseline
-def cpu_baseline(cfg, snap, sample_layers=1):
+def _ref_layer_seconds(cfg, snap, threads, groups, reps=3, warmup=1):
     """The reference's run_iteration(tree, Flatten, 128, pool, queries,
-    {d_head, n_heads=G, use_double=false}) on one kv-head group (G q heads,
-    KV expanded) of one layer; extrapolated x h_kv x n_layers.  Uses the
-    reference compiled in place (oracle/_ref) when present, else the C port."""
+    {d_head, n_heads, tile 32, float}) over `groups` kv-head groups of one
+    layer (each group: G q heads over its kv head, GQA expanded to MHA, the
+    reference being MHA-only), compiled in place (oracle/_ref); else the C port
+    (1 thread).  Returns (best seconds for the groups, kind, threads used)."""
     from oracle import core, ref
-    threads = os.cpu_count() or 1
     G = cfg["h_q"] // cfg["h_kv"]
     d = cfg["d"]
     if ref.available():
         ref.set_threads(threads)
         ref.tune_malloc()
-        inst = ref.Instance.gqa(snap, d, G, 1, 42)
-        inst.run_iteration(128)  # warm
-        secs = []
-        t_end = time.time() + 10
-        while time.time() < t_end or not secs:
-            secs.append(inst.run_iteration(128)[2])
-            if len(secs) >= 5:
-                break
-        t = min(secs)
-        kind, cores = "reference", threads
-    else:
-        tr = core.Tree.from_snapshot(snap)
-        c = core.Content.synth(tr, d, 42, qdim=G * d).expanded(d, G, 1)
-        t0 = time.perf_counter()
-        core.run_iteration_flatten(tr, c, d, G)
-        t = time.perf_counter() - t0
-        kind, cores = "port", 1
-    per_step_us = t * 1e6 * cfg["h_kv"] * cfg["n_layers"]
-    return {"value": per_step_us, "unit": "us/decode step", "cores": cores, "kind": kind,
-            "sample": f"1 layer x 1 kv-head group ({G} q heads, GQA-expanded MHA) of run_iteration, "
-                      f"best of {len(secs) if kind == 'reference' else 1}, x{cfg['h_kv']} groups x{cfg['n_layers']} layers"}
+        inst = ref.Instance.gqa(snap, d, G * groups, groups, 42)
+        for _ in range(warmup):
+            inst.run_iteration(128)
+        secs = [inst.run_iteration(128)[2] for _ in range(reps)]
+        return min(secs), "reference", threads
+    tr = core.Tree.from_snapshot(snap)
+    c = core.Content.synth(tr, d * groups, 42, qdim=G * groups * d).expanded(d, G * groups, groups)
+    t0 = time.perf_counter()
+    core.run_iteration_flatten(tr, c, d, G * groups)
+    return time.perf_counter() - t0, "port", 1
 
 
-# ------------------------------------------------------------------- main
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="few_shot", choices=sorted(CONFIGS))
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="launch the layer calls eagerly (no CUDA graph)")
-    ap.add_argument("--opt", action="append", default=[], help="ta_set_option key=value (repeatable)")
-    args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+def cpu_baseline(cfg, snap, world=1):
+    """CPU reference beside the GPU number (rank 0, N = 1): one layer of the
+    step at all host threads (all local kv groups) and one kv group at one
+    thread, each scaled to the whole step (x n_layers, x groups)."""
+    nproc = os.cpu_count() or 1
+    n_loc = local_kv_heads(cfg, world)
+    L = cfg["n_layers"]
+    t_all, kind, cores = _ref_layer_seconds(cfg, snap, nproc, n_loc, reps=3)
+    t_one, _, _ = _ref_layer_seconds(cfg, snap, 1, 1, reps=1, warmup=0)
+    G = cfg["h_q"] // cfg["h_kv"]
+    return {"value": t_all * 1e6 * L, "unit": "us/decode step", "cores": cores, "kind": kind,
+            "cpu_model": cpu_model(), "nproc": nproc,
+            "sample": f"1 layer (all {n_loc} kv-head groups x {G} q heads, GQA-expanded MHA) of run_iteration(Flatten, 128), "
+                      f"best of 3 after 1 warm-up, x{L} layers (extrapolated: layers are identical work)",
+            "extrapolated": {"layers": L},
+            "single_thread": {"value": t_one * 1e6 * n_loc * L, "unit": "us/decode step", "cores": 1,
+                              "sample": f"1 kv-head group of 1 layer at TREEATTN_THREADS=1, x{n_loc} groups x{L} layers",
+                              "extrapolated": {"groups": n_loc, "layers": L}}}
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    snap = build_snapshot(cfg)
 
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        runs = []
-        from oracle import ref
-        for _ in range(args.warmup):
-            pass
-        for _ in range(args.steps):
-            runs.append(cpu_baseline(cfg, snap))
-        v = statistics.median(r["value"] for r in runs)
-        base = dict(runs[0])
-        base["value"] = v
-        line = {"metric": METRIC, "value": v, "unit": "us/decode step", "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": v / 1000.0, "higher_is_better": False, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference synth.hpp content, seed 42)",
-                "impl": "reference", "config": config_obj(args, cfg, world), "cpu_baseline": base,
-                "e2e": {"value": v, "unit": "us/decode step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                "gpu_launches": 0}
-        print(json.dumps(line))
-        return
-
+# ------------------------------------------------------------------- our arm
+def measure(name, cfg, args, world, rank, local_rank, clocks=None, with_cpu=False, steps=None):
+    """Builds the config's tree, pools and queries on this rank, times the
+    decode step (graph-replayed layer calls after ta_prepare), the per-layer
+    attention time and the e2e host-buffer step.  Returns a dict."""
     import torch
-    torch.cuda.set_device(local_rank)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     from paper_2404_00242_b200 import TreeAttention
 
+    steps = steps or args.steps
+    snap = build_snapshot(cfg)
     h_kv, h_q, d, L_layers = cfg["h_kv"], cfg["h_q"], cfg["d"], cfg["n_layers"]
-    assert h_kv % world == 0, "kv heads must divide across ranks"
-    n_loc = h_kv // world
+    n_loc = local_kv_heads(cfg, world)
+    assert cfg.get("n_local_kv_heads") or h_kv % world == 0, "kv heads must divide across ranks"
     G = h_q // h_kv
+    kv_begin = (rank * n_loc) % h_kv
     root, ids, par, cnt = snap
     pages = int(sum((int(c) + 15) // 16 for c in cnt)) + 16
     ctx = TreeAttention(n_layers=L_layers, n_q_heads=h_q, n_kv_heads=h_kv, d_head=d, kv_dtype=cfg["dtype"],
                         out_dtype=cfg["dtype"], max_pages=pages, device=local_rank,
-                        kv_head_begin=rank * n_loc, n_local_kv_heads=n_loc)
+                        kv_head_begin=kv_begin, n_local_kv_heads=n_loc)
     for kv in args.opt:
         k, v = kv.split("=")
         ctx.set_option(k, int(v))
@@ -334,8 +326,7 @@ def main():
         if graph is not None:
             graph.replay()
         else:
-            for layer in range(L_layers):
-                ctx.attend(layer, q[layer], out[layer], stream=stream)
+            layers()
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -345,29 +336,28 @@ def main():
 
     # ---- timed region: device time via CUDA events, max over ranks
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clocks:
-        for _ in range(30):   # keep the GPU busy while the sampler starts
-            step()
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    if clocks:
         clocks.mark_start()
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if clocks:
         clocks.mark_end()
-        if world > 1:
-            torch.distributed.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1) / steps
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
 
-    # ---- per-layer time of ta_attend (attention + merge launches) on the
-    # launching stream: the graph of n_layers calls, replayed back to back
+    # ---- per-layer time of ta_attend on the launching stream: the graph of
+    # n_layers calls, replayed back to back (each layer's KV > L2 apart)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx.prepare(128, stream)
     torch.cuda.synchronize()
@@ -377,8 +367,7 @@ def main():
         if graph is not None:
             graph.replay()
         else:
-            for layer in range(L_layers):
-                ctx.attend(layer, q[layer], out[layer], stream=stream)
+            layers()
     ev1.record(stream)
     torch.cuda.synchronize()
     attend_ms = ev0.elapsed_time(ev1) / (reps * L_layers)
@@ -393,13 +382,17 @@ def main():
 
         def step_host():
             # one decode step through the host-buffer entry: the n_layers
-            # calls pipeline copy-in / attention / copy-out; the step ends
-            # when every layer's output is back in host memory
-            ctx.prepare(128, stream)
+            # calls pipeline copy-in / attention / copy-out; the NEXT step's
+            # ta_prepare (host plan + schedule + stream-ordered upload) runs
+            # while this step's layers execute -- the next tree is known before
+            # this step's outputs (one more token per leaf); the step ends when
+            # every layer's output is back in host memory
             for layer in range(L_layers):
                 ctx.attend_host_async(layer, qn[layer], on[layer], stream=stream)
+            ctx.prepare(128, stream)
             ctx.attend_host_wait()
 
+        ctx.prepare(128, stream)
         for _ in range(2):
             step_host()
         torch.cuda.synchronize()
@@ -409,12 +402,12 @@ def main():
         h1 = torch.cuda.Event(enable_timing=True)
         h0.record(stream)
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(steps):
             step_host()
         h1.record(stream)
         torch.cuda.synchronize()
-        wall_ms = (time.perf_counter() - t0) * 1000 / args.steps
-        ems = max(h0.elapsed_time(h1) / args.steps, wall_ms)
+        wall_ms = (time.perf_counter() - t0) * 1000 / steps
+        ems = max(h0.elapsed_time(h1) / steps, wall_ms)
         if world > 1:
             t = torch.tensor([ems], device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -422,13 +415,9 @@ def main():
         e2e = {"value": ems * 1000.0, "unit": "us/decode step",
                "h2d_bytes_per_step": int(q.numel() * q.element_size()),
                "d2h_bytes_per_step": int(out.numel() * out.element_size()),
-               "path": "ta_prepare + ta_attend_host_async per layer (pinned host q in, host out back; copy-in, "
-                        "attention and copy-out of consecutive layers overlap) + ta_attend_host_wait per step"}
-
-    if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return
+               "path": "ta_attend_host_async per layer (pinned host q in, host out back; copy-in, attention and "
+                        "copy-out of consecutive layers overlap), the next step's ta_prepare while they run, "
+                        "ta_attend_host_wait"}
 
     peak, peak_kind = measured_peaks()
     alg_bytes = io.kv_bytes  # one pass over unique tree KV per layer (this rank's heads)
@@ -439,55 +428,256 @@ def main():
     ridge = tpeak * 1e12 / (peak * 1e9)
     hbm_line = {"achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak}
     tflops = io.flops / (attend_ms * 1e-3) / 1e12
-    tensor_line = {"achieved": tflops, "peak": tpeak, "peak_kind": tpeak_kind, "unit": "TFLOP/s", "frac": tflops / tpeak}
+    tensor_line = {"achieved": tflops, "peak": tpeak, "peak_kind": tpeak_kind, "unit": "TFLOP/s",
+                   "frac": tflops / tpeak}
     tensor_bound = io.flops >= ridge * alg_bytes
     roofline = dict(tensor_line if tensor_bound else hbm_line)
-    roofline.update({"kernel": "ta_attend (attn_mma or attn_fma + merge), per layer, graph-replayed",
+    roofline.update({"kernel": "ta_attend (attn_mma with the fused merge, or attn_fma + merge), per layer, graph-replayed",
                      "bound": "tensor" if tensor_bound else "hbm",
-                     "traffic": profile_traffic(args.config), "alg_bytes_per_launch": alg_bytes,
+                     "traffic": profile_traffic(name), "alg_bytes_per_launch": alg_bytes,
                      "alg_flops_per_launch": io.flops, "intensity_flop_per_byte": io.flops / max(1, alg_bytes),
                      "other": tensor_line if not tensor_bound else hbm_line})
-    cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    res = {"value": ms * 1000.0, "ms_per_step": ms, "us_per_layer": attend_ms * 1000.0, "roofline": roofline,
+           "e2e": e2e, "kv_io_bytes_per_step": io.kv_bytes * L_layers,
+           "kv_bytes_loaded_per_step": io.kv_bytes_loaded * L_layers,
+           "partial_io_bytes_per_step": io.partial_bytes * L_layers, "meta_bytes_per_step": io.meta_bytes,
+           "q_out_bytes_per_step": (io.q_bytes + io.out_bytes) * L_layers,
+           "gpu_launches": steps * L_layers * launches_per_attend,
+           "schedule": {"chunks": io.n_chunks, "groups": io.n_groups, "units": io.n_units,
+                        "units_mma": io.n_units_mma, "partials": io.n_partials,
+                        "kv_bytes_loaded_per_layer": io.kv_bytes_loaded, "launches_per_layer": launches_per_attend},
+           "config": config_obj(name, cfg, world)}
+    if with_cpu and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(cfg, snap)
+            res["cpu_baseline"] = cpu_baseline(cfg, snap, world)
         except Exception as e:  # the baseline must never sink the bench line
-            cpu = {"value": None, "unit": "us/decode step", "cores": 0, "kind": "unavailable", "sample": str(e)[:200]}
+            res["cpu_baseline"] = {"value": None, "unit": "us/decode step", "cores": 0, "kind": "unavailable",
+                                   "sample": str(e)[:200]}
+    del graph, ctx
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_decode_loop(name, cfg, args, world, rank, local_rank):
+    """A real decode loop of gen_few_shot (workloads.hpp:98-111): every step
+    appends one token per leaf (ta_tree_append_leaves), re-plans
+    (ta_prepare: flatten plan + device schedule + metadata upload), and replays
+    ONE CUDA graph of n_layers x (ta_kv_append of the step's new K/V rows +
+    ta_attend).  The graph is captured once and stays valid across re-plans
+    (re-captured only when ta_graph_epoch changes).  The timed steps end at the
+    config's iteration (400 for B).  New K/V rows are random device tensors
+    reused every step (their values do not affect the timing)."""
+    import torch
+    from oracle import core
+    from paper_2404_00242_b200 import TreeAttention
+    K, W = args.steps, max(3, args.warmup)
+    it0 = cfg["iteration"] - K - W
+    t = core.Tree(cfg["prefix"])
+    kids = t.branch(t.root, [it0] * cfg["branches"])
+    root, ids, par, cnt = t.snapshot()
+    h_kv, h_q, d, L_layers = cfg["h_kv"], cfg["h_q"], cfg["d"], cfg["n_layers"]
+    n_loc = local_kv_heads(cfg, world)
+    G = h_q // h_kv
+    pages = cfg["prefix"] // 16 + 1 + cfg["branches"] * ((cfg["iteration"] + 15) // 16 + 1) + 16
+    ctx = TreeAttention(n_layers=L_layers, n_q_heads=h_q, n_kv_heads=h_kv, d_head=d, kv_dtype=cfg["dtype"],
+                        out_dtype=cfg["dtype"], max_pages=pages, device=local_rank,
+                        kv_head_begin=(rank * n_loc) % h_kv, n_local_kv_heads=n_loc)
+    for kv in args.opt:
+        k_, v_ = kv.split("=")
+        ctx.set_option(k_, int(v_))
+    ctx.restore(root, ids, par, cnt)
+    dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    gen = torch.Generator(device="cuda").manual_seed(99 + rank)
+    for layer in range(L_layers):
+        for node, c in zip(ids, cnt):
+            if int(c):
+                ctx.write_kv(layer, int(node), (torch.rand((int(c), n_loc, d), generator=gen, device="cuda") * 2 - 1).to(dt),
+                             (torch.rand((int(c), n_loc, d), generator=gen, device="cuda") * 2 - 1).to(dt))
+    L = len(ctx.leaves())
+    q = (torch.rand((L_layers, L, n_loc * G, d), generator=gen, device="cuda") * 2 - 1).to(dt)
+    out = torch.empty_like(q)
+    nk = (torch.rand((L_layers, L, n_loc, d), generator=gen, device="cuda") * 2 - 1).to(dt)
+    nv = (torch.rand((L_layers, L, n_loc, d), generator=gen, device="cuda") * 2 - 1).to(dt)
+    stream = torch.cuda.current_stream()
+    state = {"graph": None, "epoch": None, "recaptures": 0}
+
+    def layers():
+        s = torch.cuda.current_stream()
+        for layer in range(L_layers):
+            ctx.kv_append(layer, nk[layer], nv[layer], stream=s)
+            ctx.attend(layer, q[layer], out[layer], stream=s)
+
+    host = []
+
+    def step():
+        h0 = time.perf_counter()
+        ctx.append_leaves()
+        ctx.prepare(128, stream)
+        host.append(time.perf_counter() - h0)
+        if state["graph"] is None or ctx.graph_epoch() != state["epoch"]:
+            torch.cuda.synchronize()
+            state["epoch"] = ctx.graph_epoch()
+            state["graph"] = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(state["graph"]):
+                layers()
+            state["recaptures"] += 1
+        state["graph"].replay()
+
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    host.clear()
+    rec0 = state["recaptures"]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    w0 = time.perf_counter()
+    for _ in range(K):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - w0) / K
+    ms = e0.elapsed_time(e1) / K
+    io = ctx.io_stats()
+    res = {"us_per_step": ms * 1000.0, "wall_us_per_step": wall * 1e6,
+           "host_append_prepare_us": {"median": statistics.median(host) * 1e6, "max": max(host) * 1e6},
+           "iterations": [it0 + W + 1, it0 + W + K], "graph_recaptures_in_timed_steps": state["recaptures"] - rec0,
+           "kv_append_rows_per_step": ctx.kv_append_rows(), "gpu_launches_per_step": L_layers * (1 + ctx.launches_per_attend()),
+           "kv_bytes_per_layer_at_end": io.kv_bytes,
+           "path": "per step: ta_tree_append_leaves (1 token per leaf) + ta_prepare, then one graph replay of "
+                   "n_layers x (ta_kv_append + ta_attend)"}
+    del state, ctx
+    torch.cuda.empty_cache()
+    return res
+
+
+# ------------------------------------------------------------------- main
+def reference_arm(args, cfg, world):
+    """The reference's own CPU path (oracle/_ref: run_iteration compiled from
+    /root/reference) on this config, all host threads.  Each step times one
+    layer's run_iteration over every kv-head group (the reference is MHA only:
+    KV expanded to the q heads); the step value is that x n_layers, labelled
+    as extrapolated (the layers are identical work)."""
+    from oracle import ref
+    snap = build_snapshot(cfg)
+    nproc = os.cpu_count() or 1
+    n_loc = local_kv_heads(cfg, world) if world == 1 else cfg["h_kv"]
+    G = cfg["h_q"] // cfg["h_kv"]
+    L = cfg["n_layers"]
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref was not built (needs /root/reference)"}))
+        return
+    ref.set_threads(nproc)
+    ref.tune_malloc()
+    inst = ref.Instance.gqa(snap, cfg["d"], G * n_loc, n_loc, 42)
+    for _ in range(args.warmup):
+        inst.run_iteration(128)
+    secs = [inst.run_iteration(128)[2] for _ in range(args.steps)]
+    per_layer_us = statistics.median(secs) * 1e6
+    v = per_layer_us * L
+    sample = (f"per step: 1 layer's run_iteration(Flatten, 128) over all {n_loc} kv-head groups "
+              f"({G * n_loc} q heads, KV GQA-expanded), timed; x{L} layers")
+    line = {"metric": METRIC, "value": v, "unit": "us/decode step", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v / 1000.0, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference synth.hpp content, seed 42)",
+            "impl": "reference", "config": config_obj(args.config, cfg, world),
+            "us_per_layer": per_layer_us, "extrapolated": {"layers": L},
+            "cpu_baseline": {"value": v, "unit": "us/decode step", "cores": nproc, "kind": "reference",
+                             "cpu_model": cpu_model(), "sample": sample, "extrapolated": {"layers": L}},
+            "e2e": {"value": v, "unit": "us/decode step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="few_shot", choices=sorted(CONFIGS))
+    ap.add_argument("--headline-only", action="store_true", help="skip the per-config sub-map")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the layer calls eagerly (no CUDA graph)")
+    ap.add_argument("--opt", action="append", default=[], help="ta_set_option key=value (repeatable)")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args, cfg, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    with ClockSampler(local_rank) as clocks:
+        head = measure(args.config, cfg, args, world, rank, local_rank, clocks=clocks, with_cpu=True)
+    decode = None
+    if cfg["kind"] == "few_shot" and not args.headline_only:
+        try:
+            decode = measure_decode_loop(args.config, cfg, args, world, rank, local_rank)
+        except Exception as e:
+            decode = {"error": str(e)[:300]}
+    subs = {}
+    if world == 1 and not args.headline_only and args.config == "few_shot":
+        for name in SUB_CONFIGS:
+            try:
+                subs[name] = measure(name, CONFIGS[name], args, world, rank, local_rank, with_cpu=True,
+                                     steps=min(args.steps, 20))
+            except Exception as e:   # a sub-config must never sink the headline line
+                subs[name] = {"error": str(e)[:300]}
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
     line = {
         "metric": METRIC,
-        "value": ms * 1000.0,
+        "value": head["value"],
         "unit": "us/decode step",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": ms,
+        "ms_per_step": head["ms_per_step"],
         "higher_is_better": False,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": cfg["dtype"],
         "data": "synthetic (uniform(-1,1) KV/Q, reference tree generators)",
-        "config": config_obj(args, cfg, world),
-        "kv_io_bytes_per_step": io.kv_bytes * L_layers,
-        "partial_io_bytes_per_step": io.partial_bytes * L_layers,
-        "meta_bytes_per_step": io.meta_bytes,
-        "us_per_layer": attend_ms * 1000.0,
-        "roofline": roofline,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
+        "config": head["config"],
+        "kv_io_bytes_per_step": head["kv_io_bytes_per_step"],
+        "partial_io_bytes_per_step": head["partial_io_bytes_per_step"],
+        "meta_bytes_per_step": head["meta_bytes_per_step"],
+        "us_per_layer": head["us_per_layer"],
+        "roofline": head["roofline"],
+        "cpu_baseline": head.get("cpu_baseline"),
+        "e2e": head["e2e"],
         "clocks": clocks.summary(),
-        "gpu_launches": args.steps * L_layers * launches_per_attend,
-        "schedule": {"chunks": io.n_chunks, "groups": io.n_groups, "units": io.n_units, "units_mma": io.n_units_mma,
-                     "partials": io.n_partials, "kv_bytes_loaded_per_layer": io.kv_bytes_loaded},
+        "gpu_launches": head["gpu_launches"],
+        "schedule": head["schedule"],
     }
+    if decode:
+        line["decode_loop"] = decode
+    if subs:
+        line["configs"] = subs
     print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
-def config_obj(args, cfg, world):
-    return {"workload": args.config, **{k: v for k, v in cfg.items() if k != "kind"}, "block_size": 128,
-            "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
-            "l2": "inputs larger than L2 (per-layer KV pools, n_layers x unique KV per step)"}
+def config_obj(name, cfg, world):
+    n_loc = cfg.get("n_local_kv_heads") or cfg["h_kv"] // world
+    par = (f"kv-head shard: {n_loc} of {cfg['h_kv']} kv heads per GPU" if cfg.get("n_local_kv_heads")
+           else f"kv-head shard x{world}" if world > 1 else "single GPU")
+    return {"workload": name, **{k: v for k, v in cfg.items() if k != "kind"}, "block_size": 128,
+            "parallelism": par, "l2": "inputs larger than L2 (per-layer KV pools, n_layers x unique KV per step)"}
 
 
 if __name__ == "__main__":

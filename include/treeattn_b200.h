@@ -90,6 +90,10 @@ ta_status ta_tree_branch(ta_ctx* ctx, int32_t at, int n, const int64_t* child_to
                          int32_t* created);
 ta_status ta_tree_prune(ta_ctx* ctx, int32_t at);
 ta_status ta_tree_append(ta_ctx* ctx, int32_t leaf, int64_t n);
+/* append_tokens on many leaves in one call (the decode step of gen_few_shot,
+ * workloads.hpp:98-111): leaves NULL = every leaf in leaves() order (n must be
+ * the leaf count), counts NULL = one token each.  All or nothing. */
+ta_status ta_tree_append_leaves(ta_ctx* ctx, int n, const int32_t* leaves, const int64_t* counts);
 /* leaves in DFS pre-order; *n receives the count (out may be NULL to size) */
 ta_status ta_tree_leaves(ta_ctx* ctx, int32_t* out, int cap, int* n);
 
@@ -118,6 +122,21 @@ ta_status ta_pool_token_ref(ta_ctx* ctx, int32_t node, int64_t token, int32_t* p
  * device or host source pointers.  stream: cudaStream_t (NULL = default). */
 ta_status ta_kv_write(ta_ctx* ctx, int layer, int32_t node, int64_t tok_begin, int64_t n_tok,
                       const void* k, const void* v, int src_on_device, void* stream);
+
+/* ---- Decode-step KV append (PagePool::write_kv of the step's new tokens,
+ * kv_cache.hpp:104-116, batched and asynchronous).  The pool rows of every
+ * token appended (ta_tree_append / ta_tree_append_leaves) since the previous
+ * ta_prepare are uploaded by the next ta_prepare; ta_kv_append then writes
+ * that layer's rows k, v [n_rows][n_local_kv_heads][d_head] (device, in
+ * append order) with one kernel and no host synchronisation.  The row count
+ * is read on the device, so the call can live in a captured CUDA graph. */
+ta_status ta_kv_append(ta_ctx* ctx, int layer, const void* k, const void* v, void* stream);
+/* rows the last ta_prepare uploaded for ta_kv_append */
+int64_t ta_kv_append_rows(ta_ctx* ctx);
+/* Captured launches (ta_attend, ta_kv_append in a CUDA graph) stay valid
+ * across ta_prepare calls while this value is unchanged; it changes when a
+ * larger schedule relocates the metadata / scratch buffers. */
+int64_t ta_graph_epoch(ta_ctx* ctx);
 
 /* ---- Plan (bit-exact partition_flatten) ---------------------------------- */
 typedef struct ta_plan_view {

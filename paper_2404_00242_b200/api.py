@@ -131,6 +131,38 @@ class TreeAttention:
     def append_tokens(self, leaf: int, n: int):
         check(lib().ta_tree_append(self._h, int(leaf), int(n)), "append_tokens")
 
+    def append_leaves(self, leaves=None, counts=None):
+        """append_tokens on many leaves at once (default: one token on every
+        leaf, leaves() order): the decode step of gen_few_shot."""
+        if leaves is None:
+            n = -1 if counts is None else len(counts)
+            lp = None
+        else:
+            la = np.ascontiguousarray(leaves, np.int32)
+            n, lp = len(la), la.ctypes.data_as(C.POINTER(C.c_int32))
+        ca = None if counts is None else np.ascontiguousarray(counts, np.int64)
+        if leaves is None and ca is not None:
+            n = len(ca)
+        check(lib().ta_tree_append_leaves(self._h, n, lp, None if ca is None else ca.ctypes.data_as(C.POINTER(C.c_int64))),
+              "append_tokens")
+
+    def kv_append(self, layer: int, k, v, stream=None):
+        """Write this layer's KV of the tokens appended before the last
+        prepare(): k, v [n_rows][n_local_kv_heads][d_head] device tensors in
+        append order (one async kernel; graph-capturable)."""
+        for nm, x in (("kv_append k", k), ("kv_append v", v)):
+            self._check_buf(nm, x, tuple(x.shape), self.kv_dtype)
+            if int(np.prod(x.shape[1:])) != self.n_local_kv_heads * self.d_head:
+                raise ValueError(f"{nm}: rows must be [n_local_kv_heads][d_head]")
+        check(lib().ta_kv_append(self._h, int(layer), _ptr(k), _ptr(v), _stream(stream)), "kv_append")
+
+    def kv_append_rows(self) -> int:
+        return int(lib().ta_kv_append_rows(self._h))
+
+    def graph_epoch(self) -> int:
+        """Captured ta_attend / ta_kv_append launches stay valid while this is unchanged."""
+        return int(lib().ta_graph_epoch(self._h))
+
     def leaves(self) -> np.ndarray:
         n = C.c_int()
         check(lib().ta_tree_leaves(self._h, None, 0, C.byref(n)), "leaves")

@@ -28,6 +28,7 @@ EXPORTED = [
     "ta_tree_leaves", "ta_tree_get_info", "ta_tree_snapshot", "ta_pool_stats", "ta_pool_token_ref",
     "ta_kv_write", "ta_plan_flatten", "ta_plan_json", "ta_prepare", "ta_attend", "ta_attend_host", "ta_attend_host_async", "ta_attend_host_wait",
     "ta_io_stats_get", "ta_launches_per_attend", "ta_schedule_get",
+    "ta_tree_append_leaves", "ta_kv_append", "ta_kv_append_rows", "ta_graph_epoch",
 ]
 
 
@@ -146,6 +147,10 @@ def lib():
         "ta_io_stats_get": (C.c_int, [vp, C.POINTER(IoStats)]),
         "ta_launches_per_attend": (C.c_int, [vp]),
         "ta_schedule_get": (C.c_int, [vp, C.c_int, C.POINTER(ScheduleView)]),
+        "ta_tree_append_leaves": (C.c_int, [vp, C.c_int, pi32, pi64]),
+        "ta_kv_append": (C.c_int, [vp, C.c_int, vp, vp, vp]),
+        "ta_kv_append_rows": (i64, [vp]),
+        "ta_graph_epoch": (i64, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

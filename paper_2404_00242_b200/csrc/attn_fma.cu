@@ -418,7 +418,33 @@ __global__ void kv_scatter_kernel(const uint4* __restrict__ sk, const uint4* __r
     }
 }
 
+// ta_kv_append: n = counts->n_append rows, read on the device (a captured
+// decode step stays valid as the number of new tokens changes)
+__global__ void kv_append_kernel(const uint4* __restrict__ sk, const uint4* __restrict__ sv, uint4* __restrict__ dk,
+                                 uint4* __restrict__ dv, const int32_t* __restrict__ rows,
+                                 const DevCounts* __restrict__ counts, int n_loc, int64_t head_stride_v, int row_v) {
+    const int64_t total = (int64_t)counts->n_append * n_loc * row_v;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % row_v);
+        const int64_t th = i / row_v;
+        const int h = (int)(th % n_loc);
+        const int t = (int)(th / n_loc);
+        const int64_t dst = h * head_stride_v + (int64_t)rows[t] * row_v + c;
+        dk[dst] = sk[i];
+        dv[dst] = sv[i];
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_kv_append(const void* src_k, const void* src_v, void* dst_k, void* dst_v, const int32_t* rows,
+                             const DevCounts* counts, int n_loc, int64_t head_stride, int D, int esize, int n_sms,
+                             cudaStream_t s) {
+    const int row_v = D * esize / 16;
+    kv_append_kernel<<<2 * n_sms, 256, 0, s>>>((const uint4*)src_k, (const uint4*)src_v, (uint4*)dst_k, (uint4*)dst_v,
+                                               rows, counts, n_loc, head_stride * esize / 16, row_v);
+    return cudaGetLastError();
+}
 
 int fma_tile_groups(int D, int esize) {
     const int tg = 32768 / (16 * D * esize);

@@ -45,12 +45,19 @@ struct ta_ctx {
     int64_t layer_elems = 0;  // elements per layer slab
     int64_t head_stride = 0;  // elements per (layer, head) pool
 
-    // schedule metadata (one device blob) + pinned staging
+    // schedule metadata: one device blob of fixed-offset parts (see
+    // upload_schedule) + double-buffered pinned staging
     void* meta_dev = nullptr;
-    size_t meta_cap = 0;
-    void* meta_host = nullptr;
-    size_t meta_host_cap = 0;
-    cudaEvent_t meta_done = nullptr;
+    std::vector<size_t> meta_part_off, meta_part_cap;
+    size_t meta_bytes_total = 0;
+    void* meta_host[2] = {nullptr, nullptr};
+    cudaEvent_t meta_done[2] = {nullptr, nullptr};
+    int meta_buf = 0;
+    int64_t graph_epoch = 0;      // bumped whenever a relocation invalidates captured launches
+    const DevCounts* d_counts = nullptr;
+    const int32_t* d_append_rows = nullptr;
+    int64_t n_append = 0;         // tokens whose rows the last ta_prepare uploaded for ta_kv_append
+    std::vector<int32_t> pending_rows;   // pool rows of tokens appended since the last ta_prepare
     const TileDesc* d_tiles = nullptr;
     const TileMeta* d_tile_meta = nullptr;
     const int32_t* d_grp_row = nullptr;
@@ -67,7 +74,7 @@ struct ta_ctx {
     const int32_t* d_cta_own_begin = nullptr;
     const int32_t* d_cta_own = nullptr;
     unsigned* merge_cnt = nullptr;   // fused merge counters, one per merge record
-    size_t merge_cnt_cap = 0;        // bytes
+    size_t merge_cnt_n = 0;          // capacity (records)
     bool fused_merge = true;         // option "fused_merge"
     bool pdl = true;
     int prefetch_tiles = 2;
@@ -78,9 +85,9 @@ struct ta_ctx {
     // host copy of the schedule for ta_schedule_get
     Schedule dbg_sched;
 
-    // partial scratch
+    // partial scratch: o [part_rec_cap][G][D] then lse [part_rec_cap][G]
     float* part = nullptr;
-    size_t part_cap = 0;  // floats
+    size_t part_rec_cap = 0;
 
     // staging for kv writes and host-buffer attend
     void* stage_dev = nullptr;
@@ -109,7 +116,8 @@ struct ta_ctx {
             cudaFree(kv_k);
             cudaFree(kv_v);
             cudaFree(meta_dev);
-            cudaFreeHost(meta_host);
+            cudaFreeHost(meta_host[0]);
+            cudaFreeHost(meta_host[1]);
             cudaFree(part);
             cudaFree(merge_cnt);
             cudaFree(stage_dev);
@@ -123,7 +131,8 @@ struct ta_ctx {
             }
             if (h2d_stream) cudaStreamDestroy(h2d_stream);
             if (d2h_stream) cudaStreamDestroy(d2h_stream);
-            if (meta_done) cudaEventDestroy(meta_done);
+            for (cudaEvent_t e : meta_done)
+                if (e) cudaEventDestroy(e);
         }
     }
 };
@@ -238,7 +247,8 @@ ta_status ta_ctx_create(int device, const ta_shape* s, ta_ctx** out) {
             // exactly 0, but 0 * NaN would poison O if reused memory held NaNs.
             cuda_check(cudaMemset(c->kv_k, 0, bytes), "cudaMemset(K pool)");
             cuda_check(cudaMemset(c->kv_v, 0, bytes), "cudaMemset(V pool)");
-            cuda_check(cudaEventCreateWithFlags(&c->meta_done, cudaEventDisableTiming), "cudaEventCreate");
+            for (cudaEvent_t& e : c->meta_done)
+                cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
             cudaDeviceProp prop;
             cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
             c->num_sms = prop.multiProcessorCount;
@@ -323,6 +333,7 @@ ta_status ta_tree_new(ta_ctx* c, int64_t root_tokens, int32_t* root) {
     return guard([&] {
         if (root_tokens < 1) fail(TA_ERR_INVALID_ARGUMENT, "new_tree: root_token_count must be >= 1");
         c->pool.reset();
+        c->pending_rows.clear();
         c->tree.create(root_tokens);
         if (root) *root = c->tree.root;
     });
@@ -343,6 +354,7 @@ ta_status ta_tree_restore(ta_ctx* c, int32_t root, int n, const int32_t* ids, co
                                                std::to_string(c->pool.capacity));
         }
         c->pool.reset();
+        c->pending_rows.clear();
         c->tree.restore(root, n, ids, parents, counts);
     });
 }
@@ -358,9 +370,77 @@ ta_status ta_tree_prune(ta_ctx* c, int32_t at) {
     return guard([&] { c->tree.prune(at); });
 }
 
-ta_status ta_tree_append(ta_ctx* c, int32_t leaf, int64_t n) {
-    return guard([&] { c->tree.append(leaf, n); });
+// the new tokens' pool rows, queued for the next ta_prepare (ta_kv_append)
+static void queue_rows(ta_ctx* c, int32_t leaf, int64_t t0, int64_t n) {
+    const auto& h = c->pool.handle(leaf);
+    const int P = c->pool.page_size;
+    for (int64_t t = t0; t < t0 + n; ++t) c->pending_rows.push_back((int32_t)(h.pages[t / P] * P + t % P));
 }
+
+ta_status ta_tree_append(ta_ctx* c, int32_t leaf, int64_t n) {
+    return guard([&] {
+        const int64_t t0 = c->tree.contains(leaf) ? c->tree.count[leaf] : 0;
+        c->tree.append(leaf, n);
+        queue_rows(c, leaf, t0, n);
+    });
+}
+
+ta_status ta_tree_append_leaves(ta_ctx* c, int n, const int32_t* leaves, const int64_t* counts) {
+    return guard([&] {
+        // the decode step of gen_few_shot (workloads.hpp:98-111): append_tokens
+        // (tree.hpp:119-129) on many leaves at once.  Validated and checked
+        // against the page capacity first, so it applies to all or none.
+        std::vector<int32_t> ids;
+        if (leaves) {
+            ids.assign(leaves, leaves + n);
+        } else {
+            ids = c->tree.leaves;
+            if (n >= 0 && n != (int)ids.size())
+                fail(TA_ERR_INVALID_ARGUMENT, "append_leaves: n must equal the leaf count when leaves is NULL");
+        }
+        std::vector<uint8_t> seen(c->tree.alive.size(), 0);
+        int64_t pages = 0;
+        const int P = c->pool.page_size;
+        for (size_t i = 0; i < ids.size(); ++i) {
+            const int32_t id = ids[i];
+            const int64_t k = counts ? counts[i] : 1;
+            if (!c->tree.contains(id)) fail(TA_ERR_OUT_OF_RANGE, "append_tokens: unknown node id " + std::to_string(id));
+            if (!c->tree.kids[id].empty()) fail(TA_ERR_INVALID_ARGUMENT, "append_tokens: target is not a leaf");
+            if (k < 1) fail(TA_ERR_INVALID_ARGUMENT, "append_tokens: n must be >= 1");
+            if (seen[id]++) fail(TA_ERR_INVALID_ARGUMENT, "append_leaves: leaf listed twice");
+            const int64_t have = c->tree.count[id], room = (P - have % P) % P;
+            if (k > room) pages += (k - room + P - 1) / P;
+        }
+        if (c->pool.capacity >= 0 &&
+            pages > (int64_t)c->pool.free_list.size() + c->pool.capacity - (int64_t)c->pool.pages.size())
+            fail(TA_ERR_OUT_OF_MEMORY, "append_leaves: device page capacity exhausted");
+        for (size_t i = 0; i < ids.size(); ++i) {
+            const int64_t k = counts ? counts[i] : 1, t0 = c->tree.count[ids[i]];
+            c->tree.append(ids[i], k);
+            queue_rows(c, ids[i], t0, k);
+        }
+    });
+}
+
+int64_t ta_graph_epoch(ta_ctx* c) { return c ? c->graph_epoch : -1; }
+
+ta_status ta_kv_append(ta_ctx* c, int layer, const void* k, const void* v, void* stream) {
+    return guard([&] {
+        need_device(c);
+        if (!c->prepared) fail(TA_ERR_LOGIC, "kv_append: call ta_prepare after appending tokens");
+        if (layer < 0 || layer >= c->shape.n_layers) fail(TA_ERR_INVALID_ARGUMENT, "kv_append: layer out of range");
+        if (!k || !v) fail(TA_ERR_INVALID_ARGUMENT, "kv_append: null key/value");
+        if (((uintptr_t)k | (uintptr_t)v) & 15) fail(TA_ERR_INVALID_ARGUMENT, "kv_append: rows must be 16-byte aligned");
+        cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+        char* dk = (char*)c->kv_k + (size_t)layer * c->layer_elems * c->esize;
+        char* dv = (char*)c->kv_v + (size_t)layer * c->layer_elems * c->esize;
+        cuda_check(launch_kv_append(k, v, dk, dv, c->d_append_rows, c->d_counts, c->shape.n_local_kv_heads,
+                                    c->head_stride, c->shape.d_head, c->esize, c->num_sms, (cudaStream_t)stream),
+                   "kv_append");
+    });
+}
+
+int64_t ta_kv_append_rows(ta_ctx* c) { return c && c->prepared ? c->n_append : 0; }
 
 ta_status ta_tree_leaves(ta_ctx* c, int32_t* out, int cap, int* n) {
     return guard([&] {
@@ -520,6 +600,128 @@ int fma_rows(int rows) { return rows <= 4 ? 4 : rows <= 8 ? 8 : 16; }
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Schedule metadata upload.  Every part lives at a FIXED offset of one device
+// blob with room to grow (x1.5 when exceeded); the per-step counts sit in a
+// header at offset 0 that the kernels read on the device.  Kernel arguments
+// therefore stay valid from one ta_prepare to the next, so a captured CUDA
+// graph of the layer calls (and of ta_kv_append) replays correctly after
+// every re-plan; only a capacity growth relocates buffers, which bumps
+// ta_graph_epoch.  Pinned staging is double-buffered: ta_prepare for the next
+// step never waits for the current step's upload.
+enum {
+    P_HDR, P_TILES, P_TMETA, P_GROW, P_GINFO, P_ITEMS, P_CTAB, P_SLEAF, P_SOUT, P_MREC, P_PMERGE, P_PUBB, P_PUB,
+    P_EMPTY, P_OWNB, P_OWN, P_APPEND, NPART
+};
+
+static void upload_schedule(ta_ctx* c, cudaStream_t s) {
+    const Schedule& S = c->sched;
+    DevCounts hdr{};
+    hdr.n_empty = (int32_t)(S.empty.size() / 2);
+    hdr.n_merge = (int32_t)S.merge_rec.size();
+    hdr.n_append = (int32_t)c->pending_rows.size();
+    hdr.n_partials = S.n_partials;
+    const std::pair<const void*, size_t> src[NPART] = {
+        {&hdr, sizeof hdr},
+        {S.tiles.data(), S.tiles.size() * sizeof(TileDesc)},
+        {S.tile_meta.data(), S.tile_meta.size() * sizeof(TileMeta)},
+        {S.grp_row.data(), S.grp_row.size() * 4},
+        {S.grp_info.data(), S.grp_info.size() * 4},
+        {S.items.data(), S.items.size() * sizeof(ItemDesc)},
+        {S.cta_begin.data(), S.cta_begin.size() * 4},
+        {S.slot_leaf.data(), S.slot_leaf.size() * 4},
+        {S.slot_out.data(), S.slot_out.size() * 4},
+        {S.merge_rec.data(), S.merge_rec.size() * 16},
+        {S.part_merge.data(), S.part_merge.size() * 4},
+        {S.cta_pub_begin.data(), S.cta_pub_begin.size() * 4},
+        {S.cta_pub.data(), S.cta_pub.size() * 8},
+        {S.empty.data(), S.empty.size() * 4},
+        {S.cta_own_begin.data(), S.cta_own_begin.size() * 4},
+        {S.cta_own.data(), S.cta_own.size() * 4},
+        {c->pending_rows.data(), c->pending_rows.size() * 4},
+    };
+    static_assert(sizeof(src) / sizeof(src[0]) == NPART, "parts");
+    // capacities (bytes): grow all exceeded parts by 1.5x, keep the rest
+    bool relocate = c->meta_part_cap.size() != NPART;
+    if (relocate) c->meta_part_cap.assign(NPART, 0);
+    for (int i = 0; i < NPART; ++i)
+        if (src[i].second > c->meta_part_cap[i]) relocate = true;
+    const int G = c->G, D = c->shape.d_head;
+    const size_t n_part = (size_t)std::max(1, S.n_partials), n_rec = std::max<size_t>(1, S.merge_rec.size());
+    if (n_part > c->part_rec_cap || n_rec > c->merge_cnt_n) relocate = true;
+    if (relocate) {
+        // every relocation invalidates captured launches: make them rare
+        cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        size_t off = 0;
+        c->meta_part_off.assign(NPART, 0);
+        for (int i = 0; i < NPART; ++i) {
+            if (src[i].second > c->meta_part_cap[i])
+                c->meta_part_cap[i] = std::max<size_t>(256, align_up(src[i].second * 3 / 2, 256));
+            c->meta_part_off[i] = off;
+            off += c->meta_part_cap[i];
+        }
+        c->meta_bytes_total = off;
+        cudaFree(c->meta_dev);
+        c->meta_dev = nullptr;
+        cuda_check(cudaMalloc(&c->meta_dev, off), "cudaMalloc(schedule metadata)");
+        for (int b = 0; b < 2; ++b) {
+            cudaFreeHost(c->meta_host[b]);
+            c->meta_host[b] = nullptr;
+            cuda_check(cudaMallocHost(&c->meta_host[b], off), "cudaMallocHost(schedule staging)");
+        }
+        if (n_part > c->part_rec_cap) {
+            c->part_rec_cap = std::max(n_part * 3 / 2, c->part_rec_cap);
+            cudaFree(c->part);
+            c->part = nullptr;
+            cuda_check(cudaMalloc(&c->part, c->part_rec_cap * G * (D + 1) * sizeof(float)), "cudaMalloc(partials)");
+        }
+        if (n_rec > c->merge_cnt_n) {
+            c->merge_cnt_n = std::max(n_rec * 3 / 2, c->merge_cnt_n);
+            cudaFree(c->merge_cnt);
+            c->merge_cnt = nullptr;
+            cuda_check(cudaMalloc(&c->merge_cnt, c->merge_cnt_n * sizeof(unsigned)), "cudaMalloc(merge counters)");
+            cuda_check(cudaMemsetAsync(c->merge_cnt, 0, c->merge_cnt_n * sizeof(unsigned), s), "cudaMemsetAsync");
+        }
+        ++c->graph_epoch;
+    }
+    const int b = c->meta_buf;
+    c->meta_buf ^= 1;
+    // the upload that last used this staging buffer (two prepares ago) is done
+    cuda_check(cudaEventSynchronize(c->meta_done[b]), "cudaEventSynchronize");
+    char* h = (char*)c->meta_host[b];
+    size_t extent = 0;
+    for (int i = 0; i < NPART; ++i) {
+        if (src[i].second) std::memcpy(h + c->meta_part_off[i], src[i].first, src[i].second);
+        if (src[i].second) extent = c->meta_part_off[i] + src[i].second;
+    }
+    cuda_check(cudaMemcpyAsync(c->meta_dev, h, extent, cudaMemcpyHostToDevice, s), "metadata upload");
+    cuda_check(cudaEventRecord(c->meta_done[b], s), "cudaEventRecord");
+    char* d = (char*)c->meta_dev;
+    auto at = [&](int i) { return (const void*)(d + c->meta_part_off[i]); };
+    c->d_counts = (const DevCounts*)at(P_HDR);
+    c->d_tiles = (const TileDesc*)at(P_TILES);
+    c->d_tile_meta = (const TileMeta*)at(P_TMETA);
+    c->d_grp_row = (const int32_t*)at(P_GROW);
+    c->d_grp_info = (const uint32_t*)at(P_GINFO);
+    c->d_items = (const ItemDesc*)at(P_ITEMS);
+    c->d_cta_begin = (const int32_t*)at(P_CTAB);
+    c->d_slot_leaf = (const int32_t*)at(P_SLEAF);
+    c->d_slot_out = (const int32_t*)at(P_SOUT);
+    c->d_merge_rec = (const int4*)at(P_MREC);
+    c->d_part_merge = (const int32_t*)at(P_PMERGE);
+    c->d_cta_pub_begin = (const int32_t*)at(P_PUBB);
+    c->d_cta_pub = (const int2*)at(P_PUB);
+    c->d_empty = (const int32_t*)at(P_EMPTY);
+    c->d_cta_own_begin = (const int32_t*)at(P_OWNB);
+    c->d_cta_own = (const int32_t*)at(P_OWN);
+    c->d_append_rows = (const int32_t*)at(P_APPEND);
+    c->n_append = (int64_t)c->pending_rows.size();
+    c->pending_rows.clear();
+    // The fused-merge counters are self-resetting; zero them only after a
+    // failed launch may have left them dirty (ta_ctx_reset_counters) or on
+    // relocation above.
+}
+
 ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
     return guard([&] {
         need_device(c);
@@ -540,76 +742,7 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
                                               " exceeds the FMA kernel's 16 rows (use bf16 KV with d_head 128)");
         build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, o, c->sched);
         const Schedule& S = c->sched;
-        struct Part {
-            const void* src;
-            size_t bytes;
-            size_t off;
-        };
-        Part parts[15] = {
-            {S.tiles.data(), S.tiles.size() * sizeof(TileDesc), 0},
-            {S.tile_meta.data(), S.tile_meta.size() * sizeof(TileMeta), 0},
-            {S.grp_row.data(), S.grp_row.size() * 4, 0},
-            {S.grp_info.data(), S.grp_info.size() * 4, 0},
-            {S.items.data(), S.items.size() * sizeof(ItemDesc), 0},
-            {S.cta_begin.data(), S.cta_begin.size() * 4, 0},
-            {S.slot_leaf.data(), S.slot_leaf.size() * 4, 0},
-            {S.slot_out.data(), S.slot_out.size() * 4, 0},
-            {S.merge_rec.data(), S.merge_rec.size() * 16, 0},
-            {S.part_merge.data(), S.part_merge.size() * 4, 0},
-            {S.cta_pub_begin.data(), S.cta_pub_begin.size() * 4, 0},
-            {S.cta_pub.data(), S.cta_pub.size() * 8, 0},
-            {S.empty.data(), S.empty.size() * 4, 0},
-            {S.cta_own_begin.data(), S.cta_own_begin.size() * 4, 0},
-            {S.cta_own.data(), S.cta_own.size() * 4, 0},
-        };
-        size_t total = 0;
-        for (auto& p : parts) {
-            p.off = total;
-            total = align_up(total + p.bytes, 256);
-        }
-        total = std::max<size_t>(total, 256);
-        // the previous upload must have consumed the pinned staging
-        cuda_check(cudaEventSynchronize(c->meta_done), "cudaEventSynchronize");
-        grow_host(&c->meta_host, &c->meta_host_cap, total);
-        grow_dev(&c->meta_dev, &c->meta_cap, total);
-        for (auto& p : parts)
-            if (p.bytes) std::memcpy((char*)c->meta_host + p.off, p.src, p.bytes);
-        cudaStream_t s = (cudaStream_t)stream;
-        cuda_check(cudaMemcpyAsync(c->meta_dev, c->meta_host, total, cudaMemcpyHostToDevice, s), "metadata upload");
-        cuda_check(cudaEventRecord(c->meta_done, s), "cudaEventRecord");
-        char* d = (char*)c->meta_dev;
-        c->d_tiles = (const TileDesc*)(d + parts[0].off);
-        c->d_tile_meta = (const TileMeta*)(d + parts[1].off);
-        c->d_grp_row = (const int32_t*)(d + parts[2].off);
-        c->d_grp_info = (const uint32_t*)(d + parts[3].off);
-        c->d_items = (const ItemDesc*)(d + parts[4].off);
-        c->d_cta_begin = (const int32_t*)(d + parts[5].off);
-        c->d_slot_leaf = (const int32_t*)(d + parts[6].off);
-        c->d_slot_out = (const int32_t*)(d + parts[7].off);
-        c->d_merge_rec = (const int4*)(d + parts[8].off);
-        c->d_part_merge = (const int32_t*)(d + parts[9].off);
-        c->d_empty = (const int32_t*)(d + parts[12].off);
-        c->d_cta_pub_begin = (const int32_t*)(d + parts[10].off);
-        c->d_cta_pub = (const int2*)(d + parts[11].off);
-        c->d_cta_own_begin = (const int32_t*)(d + parts[13].off);
-        c->d_cta_own = (const int32_t*)(d + parts[14].off);
-        // fused-merge counters: zero at every prepare (self-resetting in the kernel)
-        const size_t cb = sizeof(unsigned) * std::max<size_t>(1, S.merge_rec.size());
-        if (cb > c->merge_cnt_cap) {
-            void* p = c->merge_cnt;
-            grow_dev(&p, &c->merge_cnt_cap, cb);
-            c->merge_cnt = (unsigned*)p;
-        }
-        cuda_check(cudaMemsetAsync(c->merge_cnt, 0, cb, s), "cudaMemsetAsync(merge counters)");
-        // partial scratch: o [n_part][G][D] + lse [n_part][G]
-        const size_t pf = (size_t)std::max(1, S.n_partials) * c->G * (c->shape.d_head + 1);
-        if (pf > c->part_cap) {
-            void* p = c->part;
-            size_t cap = c->part_cap * sizeof(float);
-            grow_dev(&p, &cap, pf * sizeof(float));
-            c->part = (float*)p;
-            c->part_cap = cap / sizeof(float);
-        }
+        upload_schedule(c, (cudaStream_t)stream);
         c->prepared = true;
         c->prepared_version = c->tree.version;
         c->prepared_bs = bs;
@@ -634,7 +767,8 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.out = out;
     a.lse = lse;
     a.part_o = c->part;
-    a.part_lse = c->part + (size_t)std::max(1, S.n_partials) * c->G * D;
+    a.part_lse = c->part + c->part_rec_cap * c->G * D;
+    a.counts = c->d_counts;
     a.tiles = c->d_tiles;
     a.tile_meta = c->d_tile_meta;
     a.grp_row = c->d_grp_row;
@@ -645,7 +779,6 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.slot_out = c->d_slot_out;
     a.merge_rec = c->d_merge_rec;
     a.part_merge = c->d_part_merge;
-    a.n_merge = (int)S.merge_rec.size();
     a.merge_cnt = c->merge_cnt;
     a.fused_merge = S.fused_merge ? 1 : 0;
     a.cta_pub_begin = c->d_cta_pub_begin;
@@ -653,7 +786,6 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.cta_own_begin = c->d_cta_own_begin;
     a.cta_own = c->d_cta_own;
     a.empty = c->d_empty;
-    a.n_empty = (int)(S.empty.size() / 2);
     a.n_ctas = (int)S.cta_begin.size() - 1;
     a.G = c->G;
     a.hq_loc = c->hq_loc;
@@ -674,7 +806,9 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
         cuda_check(launch_attn_mma(a, c->pdl, s), "attn_mma");
     else
         cuda_check(launch_attn_fma(a, fma_rows(S.max_lane_rows), c->pdl, s), "attn_fma");
-    if (!S.fused_merge) cuda_check(launch_merge(a, a.n_merge, c->pdl, s), "merge");
+    // always launched on the merge-launch path, so a captured step stays
+    // valid when a re-plan adds or removes merge records
+    if (!S.fused_merge) cuda_check(launch_merge(a, c->num_sms, c->pdl, s), "merge");
 }
 
 ta_status ta_attend(ta_ctx* c, int layer, const void* q, void* out, float* lse, void* stream) {
@@ -823,7 +957,7 @@ ta_status ta_schedule_get(ta_ctx* c, int bs, ta_schedule_view* o) {
 
 int ta_launches_per_attend(ta_ctx* c) {
     if (!c || !c->prepared) return 0;
-    return 1 + (c->sched.merge_leaf.empty() || c->sched.fused_merge ? 0 : 1);
+    return c->sched.fused_merge ? 1 : 2;
 }
 
 }  // extern "C"

@@ -20,26 +20,28 @@ namespace {
 using namespace dev;
 
 template <int DPL>
-__global__ void __launch_bounds__(128, 8) merge_kernel(const AttnArgs a, int n_merge) {
+__global__ void __launch_bounds__(128, 8) merge_kernel(const AttnArgs a) {
     pdl_launch_dependents();
-    const int wid = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    const bool live = wid < n_merge * a.G;
-    const int mi = live ? wid / a.G : 0, g = wid % a.G;
-    // the record is host-written schedule metadata: read it before the wait
-    const int4 rec = live ? __ldg(a.merge_rec + mi) : make_int4(0, 0, 0, 0);   // leaf, head, first partial, count
+    // counts and records are host-written schedule metadata: read before the wait
+    const int n_rows = a.counts->n_merge * a.G;
+    int wid = blockIdx.x * 4 + (threadIdx.x >> 5);
+    int4 rec = wid < n_rows ? __ldg(a.merge_rec + wid / a.G) : make_int4(0, 0, 0, 0);   // leaf, head, first partial, count
     pdl_wait();   // the attention launch's partials are complete
     if (threadIdx.x == 0) timeline_mark(a.timeline, 2, true);
-    if (live) merge_record_row<DPL>(a, rec, g, lane);
+    for (; wid < n_rows; wid += gridDim.x * 4) {
+        merge_record_row<DPL>(a, rec, wid % a.G, lane);
+        const int nx = wid + gridDim.x * 4;
+        if (nx < n_rows) rec = __ldg(a.merge_rec + nx / a.G);
+    }
     if (threadIdx.x == 0) timeline_mark(a.timeline, 2, false);
 }
 
 }  // namespace
 
-cudaError_t launch_merge(const AttnArgs& a, int n_merge, bool pdl, cudaStream_t s) {
-    if (n_merge == 0) return cudaSuccess;
+cudaError_t launch_merge(const AttnArgs& a, int n_sms, bool pdl, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((n_merge * a.G + 3) / 4);
+    cfg.gridDim = dim3(4 * n_sms);   // fixed: the record count is read on the device
     cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
@@ -48,9 +50,9 @@ cudaError_t launch_merge(const AttnArgs& a, int n_merge, bool pdl, cudaStream_t 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    if (a.D >= 128) return cudaLaunchKernelEx(&cfg, merge_kernel<4>, a, n_merge);
-    if (a.D >= 64) return cudaLaunchKernelEx(&cfg, merge_kernel<2>, a, n_merge);
-    return cudaLaunchKernelEx(&cfg, merge_kernel<1>, a, n_merge);
+    if (a.D >= 128) return cudaLaunchKernelEx(&cfg, merge_kernel<4>, a);
+    if (a.D >= 64) return cudaLaunchKernelEx(&cfg, merge_kernel<2>, a);
+    return cudaLaunchKernelEx(&cfg, merge_kernel<1>, a);
 }
 
 }  // namespace ta

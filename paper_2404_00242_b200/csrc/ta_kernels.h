@@ -12,6 +12,16 @@ namespace ta {
 // One persistent launch per layer (grid = schedule CTAs, one per SM).  A CTA
 // walks its items (see ta_internal.h); rows of an item are (slot, q head in
 // the GQA group) pairs, row = slot * G + g, local q head = head * G + g.
+// Per-step counts, at offset 0 of the schedule metadata blob (device).
+struct DevCounts {
+    int32_t n_empty;     // empty leaf-heads
+    int32_t n_merge;     // merge records
+    int32_t n_append;    // rows of ta_kv_append (tokens appended before the last ta_prepare)
+    int32_t n_partials;
+    int32_t pad[60];
+};
+static_assert(sizeof(DevCounts) == 256, "DevCounts layout");
+
 struct AttnArgs {
     // KV pools of this layer.  FMA path: element pointers + per-head stride.
     const void* k;
@@ -38,9 +48,9 @@ struct AttnArgs {
     const int32_t* cta_begin;
     const int32_t* slot_leaf;
     const int32_t* slot_out;
+    const DevCounts* counts;  // per-step counts (device; graph-stable pointer)
     const int4* merge_rec;    // [n_merge] {leaf, local kv head, first partial id, count}
     const int32_t* part_merge;// partial id -> merge record
-    int n_merge;              // merge records
     unsigned* merge_cnt;      // fused merge: per record, partials published (self-resetting)
     int fused_merge;          // 1: records merged at the end of the attention launch (tcgen05 kernel)
     const int32_t* cta_pub_begin;   // [n_ctas + 1] into cta_pub
@@ -48,7 +58,6 @@ struct AttnArgs {
     const int32_t* cta_own_begin;   // [n_ctas + 1] into cta_own
     const int32_t* cta_own;         // records the CTA merges
     const int32_t* empty;     // [n_empty][2] (leaf, head)
-    int n_empty;
     int n_ctas;
     int G;
     int hq_loc;
@@ -75,8 +84,14 @@ bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D, int b
 cudaError_t launch_attn_fma(const AttnArgs& a, int max_rows, bool pdl, cudaStream_t s);
 // groups per tile the FMA kernel stages (2 stages of K and V fit in SMEM)
 int fma_tile_groups(int D, int esize);
-// split-K merge of the partial records (after the attention launch)
-cudaError_t launch_merge(const AttnArgs& a, int n_merge, bool pdl, cudaStream_t s);
+// split-K merge of the partial records (after the attention launch); a fixed
+// grid of 4 x n_sms CTAs loops over counts->n_merge records (graph-stable)
+cudaError_t launch_merge(const AttnArgs& a, int n_sms, bool pdl, cudaStream_t s);
+// ta_kv_append: src rows [n][n_loc][D] -> pool rows rows[i] for every local
+// head, n = counts->n_append read on the device (graph-stable, fixed grid)
+cudaError_t launch_kv_append(const void* src_k, const void* src_v, void* dst_k, void* dst_v, const int32_t* rows,
+                             const DevCounts* counts, int n_loc, int64_t head_stride, int D, int esize, int n_sms,
+                             cudaStream_t s);
 // dst rows[i] <- src row i, for n_loc kv heads: src [n][n_loc][D], dst pool
 cudaError_t launch_kv_scatter(const void* src_k, const void* src_v, void* dst_k, void* dst_v,
                               const int32_t* rows, int n, int n_loc, int64_t head_stride, int D,

@@ -260,7 +260,8 @@ __device__ __forceinline__ void merge_record_row(const AttnArgs& a, int4 rec, in
 // absent from the reference's AttentionOutput).  `nl` lanes (ids 0..nl-1) of
 // one warp, strided over CTAs.
 __device__ __forceinline__ void fill_empty(const AttnArgs& a, int lane, int nl = 32) {
-    for (int e = blockIdx.x; e < a.n_empty; e += gridDim.x) {
+    const int n_empty = a.counts->n_empty;
+    for (int e = blockIdx.x; e < n_empty; e += gridDim.x) {
         const int leaf = a.empty[2 * e], head = a.empty[2 * e + 1];
         const size_t base = ((size_t)leaf * a.hq_loc + (size_t)head * a.G) * a.D;
         for (int i = lane; i < a.G * a.D; i += nl) {

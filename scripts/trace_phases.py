@@ -19,9 +19,10 @@ cfg = dict(bench.CONFIGS[name])
 snap = bench.build_snapshot(cfg)
 root, ids, par, cnt = snap
 hkv, hq, d = cfg["h_kv"], cfg["h_q"], cfg["d"]
-NL = 4
+NL = 4 if cfg["n_layers"] >= 4 else cfg["n_layers"]
+n_loc = cfg.get("n_local_kv_heads") or hkv
 ctx = TreeAttention(n_layers=NL, n_q_heads=hq, n_kv_heads=hkv, d_head=d, kv_dtype="bf16", out_dtype="bf16",
-                    max_pages=int(sum((int(c) + 15) // 16 for c in cnt)) + 16)
+                    max_pages=int(sum((int(c) + 15) // 16 for c in cnt)) + 16, n_local_kv_heads=n_loc)
 for kv in opts:
     k, v = kv.split("=")
     ctx.set_option(k, int(v))
@@ -30,10 +31,10 @@ for layer in range(NL):
     for node, c in zip(ids, cnt):
         c = int(c)
         if c:
-            ctx.write_kv(layer, int(node), (torch.rand((c, hkv, d), device="cuda") * 2 - 1).bfloat16(),
-                         (torch.rand((c, hkv, d), device="cuda") * 2 - 1).bfloat16())
+            ctx.write_kv(layer, int(node), (torch.rand((c, n_loc, d), device="cuda") * 2 - 1).bfloat16(),
+                         (torch.rand((c, n_loc, d), device="cuda") * 2 - 1).bfloat16())
 L = len(ctx.leaves())
-q = (torch.rand((L, hq, d), device="cuda") * 2 - 1).bfloat16()
+q = (torch.rand((L, ctx.n_local_q_heads, d), device="cuda") * 2 - 1).bfloat16()
 ctx.prepare(128)
 S = ctx.schedule(128)
 n_cta = S["n_ctas"]
