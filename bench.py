@@ -539,7 +539,10 @@ def measure_decode_loop(name, cfg, args, world, rank, local_rank):
     ms = e0.elapsed_time(e1) / K
     io = ctx.io_stats()
     res = {"us_per_step": ms * 1000.0, "wall_us_per_step": wall * 1e6,
-           "host_append_prepare_us": {"median": statistics.median(host) * 1e6, "max": max(host) * 1e6},
+           "host_append_prepare_us_incl_backpressure": {"median": statistics.median(host) * 1e6, "max": max(host) * 1e6},
+           "host_prepare_us": {"plan": io.host_plan_ns / 1e3, "schedule": io.host_schedule_ns / 1e3,
+                               "upload": io.host_upload_ns / 1e3,
+                               "total": (io.host_plan_ns + io.host_schedule_ns + io.host_upload_ns) / 1e3},
            "iterations": [it0 + W + 1, it0 + W + K], "graph_recaptures_in_timed_steps": state["recaptures"] - rec0,
            "kv_append_rows_per_step": ctx.kv_append_rows(), "gpu_launches_per_step": L_layers * (1 + ctx.launches_per_attend()),
            "kv_bytes_per_layer_at_end": io.kv_bytes,

@@ -55,6 +55,24 @@ enum {
 
 enum { TA_F32 = 0, TA_BF16 = 1 };
 
+/* Partition strategies (partition.hpp:16, same order).  Flatten is the hot
+ * path; the others are the paper's ablations (DeFT-Node, DeFT-Node-Chunk and
+ * the query-guided split of Flash-Decoding / Radix attention), runnable on the
+ * same kernels: select with ta_set_option(ctx, "strategy", s). */
+enum { TA_STRATEGY_Q_GUIDED = 0, TA_STRATEGY_NODE = 1, TA_STRATEGY_NODE_CHUNK = 2, TA_STRATEGY_FLATTEN = 3 };
+
+/* IO model (io_model.hpp:16-26, same order) */
+enum {
+    TA_ALG_NAIVE = 0, TA_ALG_FLASH_DECODING = 1, TA_ALG_RADIX = 2, TA_ALG_TREE_ATTN_MEDUSA = 3,
+    TA_ALG_TREE_ATTN_SPECINFER = 4, TA_ALG_NODE = 5, TA_ALG_NODE_CHUNK = 6, TA_ALG_FLATTEN = 7
+};
+typedef struct ta_cost_params {  /* CostParams (common.hpp:15-31) */
+    int d_head, n_heads, n_layers, dtype_bytes;
+} ta_cost_params;
+typedef struct ta_io_report {     /* IoReport (io_model.hpp:62-72) */
+    uint64_t kv_bytes, q_bytes, mask_bytes, partial_bytes;
+} ta_io_report;
+
 typedef struct ta_shape {
     int n_layers;        /* independent KV pools, one per layer */
     int n_q_heads;       /* h_q of the model (AttentionParams::n_heads for MHA) */
@@ -150,10 +168,17 @@ typedef struct ta_plan_view {
     const uint64_t* seg_mask;
     const int32_t* queries;     /* leaf NodeIds */
 } ta_plan_view;
-/* arrays stay valid until the next plan call on this context */
+/* The context's plan (partition_flatten unless the "strategy" option selects
+ * another partition.hpp strategy); arrays stay valid until the next plan call
+ * on this context */
 ta_status ta_plan_flatten(ta_ctx* ctx, int block_size, ta_plan_view* out);
-/* plan_to_json(partition_flatten(tree, bs)).dump(); *len excludes the NUL */
+/* plan_to_json(make_plan(tree, strategy, bs)).dump(); *len excludes the NUL */
 ta_status ta_plan_json(ta_ctx* ctx, int block_size, char* buf, size_t cap, size_t* len);
+/* io_measured(make_plan(tree, strategy, bs), params) (io_model.hpp:158-170) */
+ta_status ta_io_measured(ta_ctx* ctx, int block_size, const ta_cost_params* params, ta_io_report* out);
+/* io_analytical(tree, algorithm, params, bs) (io_model.hpp:88-153) */
+ta_status ta_io_analytical(ta_ctx* ctx, int algorithm, const ta_cost_params* params, int block_size,
+                           ta_io_report* out);
 
 /* ---- Attention ------------------------------------------------------------
  * ta_prepare: plan + device schedule + metadata upload for the current tree
@@ -193,6 +218,9 @@ typedef struct ta_io_stats {
     int64_t partial_bytes;     /* off-chip partial (m,l,O) bytes written+read per layer */
     int64_t meta_bytes;        /* schedule metadata uploaded per step */
     int64_t flops;             /* masked-in attention flops per layer (4*d per q-head-token) */
+    int64_t host_plan_ns;      /* last ta_prepare: plan (partition) time on the host */
+    int64_t host_schedule_ns;  /* ... device-schedule build */
+    int64_t host_upload_ns;    /* ... staging copy + upload enqueue (excluding any wait for the GPU) */
 } ta_io_stats;
 ta_status ta_io_stats_get(ta_ctx* ctx, ta_io_stats* out);
 

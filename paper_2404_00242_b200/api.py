@@ -62,6 +62,9 @@ class IoStats:
     partial_bytes: int
     meta_bytes: int
     flops: int
+    host_plan_ns: int
+    host_schedule_ns: int
+    host_upload_ns: int
 
 
 class TreeAttention:
@@ -265,6 +268,32 @@ class TreeAttention:
         buf = C.create_string_buffer(n.value + 1)
         check(lib().ta_plan_json(self._h, int(block_size), buf, n.value + 1, C.byref(n)), "plan_json")
         return buf.value.decode()
+
+    def set_strategy(self, name: str):
+        """Partition strategy planned by prepare / plan_json / plan_flatten:
+        "flatten" (default, the hot path), "node", "node-chunk", "q-guided"
+        (partition.hpp:16; the paper's ablations on the same kernels)."""
+        if name not in capi.TA_STRATEGY:
+            raise ValueError("unknown strategy: " + name)
+        self.set_option("strategy", capi.TA_STRATEGY[name])
+
+    def io_measured(self, block_size, d_head, n_heads, n_layers, dtype_bytes):
+        """io_measured(make_plan(tree, strategy, bs), CostParams) (io_model.hpp:158-170):
+        (kv, q, mask, partial) bytes."""
+        p = capi.CostParams(d_head, n_heads, n_layers, dtype_bytes)
+        r = capi.IoReport()
+        check(lib().ta_io_measured(self._h, int(block_size), C.byref(p), C.byref(r)), "io_measured")
+        return (r.kv_bytes, r.q_bytes, r.mask_bytes, r.partial_bytes)
+
+    def io_analytical(self, algorithm, block_size, d_head, n_heads, n_layers, dtype_bytes):
+        """io_analytical(tree, algorithm, CostParams, bs) (io_model.hpp:88-153)."""
+        if algorithm not in capi.TA_ALG:
+            raise ValueError("unknown algorithm: " + algorithm)
+        p = capi.CostParams(d_head, n_heads, n_layers, dtype_bytes)
+        r = capi.IoReport()
+        check(lib().ta_io_analytical(self._h, capi.TA_ALG[algorithm], C.byref(p), int(block_size), C.byref(r)),
+              "io_analytical")
+        return (r.kv_bytes, r.q_bytes, r.mask_bytes, r.partial_bytes)
 
     # ----------------------------------------------------------- attention
     def prepare(self, block_size: int = 128, stream=None):

@@ -29,7 +29,21 @@ EXPORTED = [
     "ta_kv_write", "ta_plan_flatten", "ta_plan_json", "ta_prepare", "ta_attend", "ta_attend_host", "ta_attend_host_async", "ta_attend_host_wait",
     "ta_io_stats_get", "ta_launches_per_attend", "ta_schedule_get",
     "ta_tree_append_leaves", "ta_kv_append", "ta_kv_append_rows", "ta_graph_epoch",
+    "ta_io_measured", "ta_io_analytical",
 ]
+
+TA_STRATEGY = {"q-guided": 0, "node": 1, "node-chunk": 2, "flatten": 3}
+TA_ALG = {"naive": 0, "flash-decoding": 1, "radix": 2, "tree-attn-medusa": 3, "tree-attn-specinfer": 4,
+          "node": 5, "node-chunk": 6, "flatten": 7}
+
+
+class CostParams(C.Structure):
+    _fields_ = [("d_head", C.c_int), ("n_heads", C.c_int), ("n_layers", C.c_int), ("dtype_bytes", C.c_int)]
+
+
+class IoReport(C.Structure):
+    _fields_ = [("kv_bytes", C.c_uint64), ("q_bytes", C.c_uint64), ("mask_bytes", C.c_uint64),
+                ("partial_bytes", C.c_uint64)]
 
 
 class TreeAttnError(Exception):
@@ -86,7 +100,8 @@ class PlanView(C.Structure):
 class IoStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "n_chunks", "n_groups", "n_units", "n_units_mma", "n_partials", "kv_bytes", "kv_bytes_loaded",
-        "q_bytes", "out_bytes", "partial_bytes", "meta_bytes", "flops")]
+        "q_bytes", "out_bytes", "partial_bytes", "meta_bytes", "flops", "host_plan_ns", "host_schedule_ns",
+        "host_upload_ns")]
 
 
 class ScheduleView(C.Structure):
@@ -151,6 +166,8 @@ def lib():
         "ta_kv_append": (C.c_int, [vp, C.c_int, vp, vp, vp]),
         "ta_kv_append_rows": (i64, [vp]),
         "ta_graph_epoch": (i64, [vp]),
+        "ta_io_measured": (C.c_int, [vp, C.c_int, C.POINTER(CostParams), C.POINTER(IoReport)]),
+        "ta_io_analytical": (C.c_int, [vp, C.c_int, C.POINTER(CostParams), C.c_int, C.POINTER(IoReport)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

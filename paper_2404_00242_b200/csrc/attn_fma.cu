@@ -423,7 +423,11 @@ __global__ void kv_scatter_kernel(const uint4* __restrict__ sk, const uint4* __r
 __global__ void kv_append_kernel(const uint4* __restrict__ sk, const uint4* __restrict__ sv, uint4* __restrict__ dk,
                                  uint4* __restrict__ dv, const int32_t* __restrict__ rows,
                                  const DevCounts* __restrict__ counts, int n_loc, int64_t head_stride_v, int row_v) {
+    // the next launch (this layer's attention) may start its prologue now; the
+    // sources (the caller's K/V projection) are ready once the previous launch is
+    pdl_launch_dependents();
     const int64_t total = (int64_t)counts->n_append * n_loc * row_v;
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int c = (int)(i % row_v);
         const int64_t th = i / row_v;
@@ -441,9 +445,17 @@ cudaError_t launch_kv_append(const void* src_k, const void* src_v, void* dst_k, 
                              const DevCounts* counts, int n_loc, int64_t head_stride, int D, int esize, int n_sms,
                              cudaStream_t s) {
     const int row_v = D * esize / 16;
-    kv_append_kernel<<<2 * n_sms, 256, 0, s>>>((const uint4*)src_k, (const uint4*)src_v, (uint4*)dst_k, (uint4*)dst_v,
-                                               rows, counts, n_loc, head_stride * esize / 16, row_v);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * n_sms);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kv_append_kernel, (const uint4*)src_k, (const uint4*)src_v, (uint4*)dst_k,
+                              (uint4*)dst_v, rows, counts, n_loc, (int64_t)(head_stride * esize / 16), row_v);
 }
 
 int fma_tile_groups(int D, int esize) {

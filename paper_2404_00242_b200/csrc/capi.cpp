@@ -4,6 +4,7 @@
 // fallback for attention.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -57,6 +58,7 @@ struct ta_ctx {
     const DevCounts* d_counts = nullptr;
     const int32_t* d_append_rows = nullptr;
     int64_t n_append = 0;         // tokens whose rows the last ta_prepare uploaded for ta_kv_append
+    int64_t t_plan_ns = 0, t_sched_ns = 0, t_upload_ns = 0;   // host time of the last ta_prepare
     std::vector<int32_t> pending_rows;   // pool rows of tokens appended since the last ta_prepare
     const TileDesc* d_tiles = nullptr;
     const TileMeta* d_tile_meta = nullptr;
@@ -76,6 +78,7 @@ struct ta_ctx {
     unsigned* merge_cnt = nullptr;   // fused merge counters, one per merge record
     size_t merge_cnt_n = 0;          // capacity (records)
     bool fused_merge = true;         // option "fused_merge"
+    int strategy = TA_STRATEGY_FLATTEN;   // option "strategy": the partition.hpp strategy planned
     bool pdl = true;
     int prefetch_tiles = 2;
     int64_t trace = 0;  // debug: device buffer for the MMA kernel's pipeline trace
@@ -189,8 +192,9 @@ void grow_host(void** p, size_t* cap, size_t need) {
 }
 
 void ensure_plan(ta_ctx* c, int bs) {
-    if (c->plan_valid && c->plan_version == c->tree.version && c->plan_bs == bs) return;
-    plan_flatten(c->tree, bs, c->plan);
+    if (c->plan_valid && c->plan_version == c->tree.version && c->plan_bs == bs && c->plan.strategy == c->strategy)
+        return;
+    make_plan(c->tree, c->strategy, bs, c->plan);
     c->plan_valid = true;
     c->plan_version = c->tree.version;
     c->plan_bs = bs;
@@ -319,6 +323,11 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->trace = v;
         } else if (k == "fused_merge") {
             c->fused_merge = v != 0;
+        } else if (k == "strategy") {
+            if (v < TA_STRATEGY_Q_GUIDED || v > TA_STRATEGY_FLATTEN)
+                fail(TA_ERR_INVALID_ARGUMENT, "strategy must be a TA_STRATEGY_* value");
+            c->strategy = (int)v;
+            c->plan_valid = false;
         } else {
             fail(TA_ERR_INVALID_ARGUMENT, "unknown option " + k);
         }
@@ -577,6 +586,94 @@ ta_status ta_plan_json(ta_ctx* c, int bs, char* buf, size_t cap, size_t* len) {
     });
 }
 
+// ------------------------------------------------------------------ IO model
+// io_measured / io_analytical (io_model.hpp:88-170) over the context's tree.
+static void check_params(const ta_cost_params* p) {
+    if (!p) fail(TA_ERR_INVALID_ARGUMENT, "CostParams: null");
+    if (p->d_head <= 0 || p->n_heads <= 0 || p->n_layers <= 0)
+        fail(TA_ERR_INVALID_ARGUMENT, "CostParams: dimensions must be positive");
+    if (p->dtype_bytes != 2 && p->dtype_bytes != 4 && p->dtype_bytes != 8)
+        fail(TA_ERR_INVALID_ARGUMENT, "CostParams: dtype_bytes must be 2, 4 or 8");
+}
+
+ta_status ta_io_measured(ta_ctx* c, int bs, const ta_cost_params* p, ta_io_report* out) {
+    return guard([&] {
+        if (c->tree.root < 0) fail(TA_ERR_LOGIC, "no tree");
+        check_params(p);
+        ensure_plan(c, bs);
+        const Plan& P = c->plan;
+        const uint64_t u = (uint64_t)p->n_heads * p->n_layers * p->dtype_bytes, d = (uint64_t)p->d_head;
+        ta_io_report r{};
+        for (int g = 0; g < P.n_groups(); ++g) {
+            uint64_t kv_len = 0;   // QkvGroup::kv_length: sum of its segment lengths
+            for (int k = P.seg_begin[g]; k < P.seg_begin[g + 1]; ++k) kv_len += (uint64_t)P.seg_len[k];
+            r.kv_bytes += 2 * d * kv_len * u;
+            r.q_bytes += (uint64_t)(P.q_begin[g + 1] - P.q_begin[g]) * d * u;
+            r.mask_bytes += (uint64_t)(P.seg_begin[g + 1] - P.seg_begin[g]) * 8 * (uint64_t)p->n_layers;
+        }
+        *out = r;   // fused execution writes no partials
+    });
+}
+
+ta_status ta_io_analytical(ta_ctx* c, int algo, const ta_cost_params* p, int bs, ta_io_report* out) {
+    return guard([&] {
+        if (c->tree.root < 0) fail(TA_ERR_LOGIC, "no tree");
+        check_params(p);
+        const Tree& t = c->tree;
+        const uint64_t u = (uint64_t)p->n_heads * p->n_layers * p->dtype_bytes, d = (uint64_t)p->d_head;
+        uint64_t n_tree = 0, live = 0, chunked = 0, sum_paths = 0;
+        for (int32_t id : t.dfs) {
+            const uint64_t tc = (uint64_t)t.count[id];
+            n_tree += tc;
+            if (tc == 0) continue;
+            live++;
+            chunked += (tc + (uint64_t)bs - 1) / (uint64_t)bs;
+        }
+        for (int32_t l : t.leaves) sum_paths += (uint64_t)t.path_tokens(l);
+        const uint64_t ln = t.leaves.size();
+        uint64_t k = 1;
+        ta_io_report r{};
+        uint64_t qkt = 0, scaled = 0, mask_add = 0, softmax = 0, dense_mask = 0;
+        switch (algo) {
+            case TA_ALG_NAIVE:
+                r.kv_bytes = 2 * d * sum_paths * u;
+                qkt = scaled = softmax = 2 * sum_paths * u;
+                break;
+            case TA_ALG_FLASH_DECODING:
+            case TA_ALG_RADIX:
+                r.kv_bytes = 2 * d * sum_paths * u;
+                break;
+            case TA_ALG_TREE_ATTN_MEDUSA:
+                r.kv_bytes = 2 * d * n_tree * u;
+                qkt = scaled = mask_add = softmax = 2 * ln * n_tree * u;
+                dense_mask = ln * n_tree * u;
+                break;
+            case TA_ALG_TREE_ATTN_SPECINFER:
+                r.kv_bytes = 2 * d * n_tree * ln * u;
+                r.mask_bytes = (ln * n_tree + 63) / 64 * u;
+                break;
+            case TA_ALG_NODE:
+                r.kv_bytes = 2 * d * n_tree * u;
+                k = live;
+                break;
+            case TA_ALG_NODE_CHUNK:
+                r.kv_bytes = 2 * d * n_tree * u;
+                k = chunked;
+                break;
+            case TA_ALG_FLATTEN:
+                r.kv_bytes = 2 * d * n_tree * u;
+                r.mask_bytes = n_tree * u;
+                k = (n_tree + (uint64_t)bs - 1) / (uint64_t)bs;
+                break;
+            default:
+                fail(TA_ERR_INVALID_ARGUMENT, "unknown algorithm " + std::to_string(algo));
+        }
+        r.partial_bytes = qkt + scaled + mask_add + softmax + dense_mask;
+        r.q_bytes = k * ln * d * u;
+        *out = r;
+    });
+}
+
 // ---------------------------------------------------------------- attention
 namespace {
 
@@ -589,6 +686,8 @@ SchedOptions effective_opts(const ta_ctx* c) {
     // at once (one CTA per SM): a record's last item then waits only for
     // items of earlier CTAs, which are running or done.
     o.fused_merge = o.use_mma && c->fused_merge && o.num_ctas <= c->num_sms;
+    // the ablation strategies run every plan group as its own stripe
+    o.fuse_chunks = c->strategy == TA_STRATEGY_FLATTEN;
     return o;
 }
 
@@ -688,6 +787,7 @@ static void upload_schedule(ta_ctx* c, cudaStream_t s) {
     c->meta_buf ^= 1;
     // the upload that last used this staging buffer (two prepares ago) is done
     cuda_check(cudaEventSynchronize(c->meta_done[b]), "cudaEventSynchronize");
+    const auto u0 = std::chrono::steady_clock::now();
     char* h = (char*)c->meta_host[b];
     size_t extent = 0;
     for (int i = 0; i < NPART; ++i) {
@@ -696,6 +796,7 @@ static void upload_schedule(ta_ctx* c, cudaStream_t s) {
     }
     cuda_check(cudaMemcpyAsync(c->meta_dev, h, extent, cudaMemcpyHostToDevice, s), "metadata upload");
     cuda_check(cudaEventRecord(c->meta_done[b], s), "cudaEventRecord");
+    c->t_upload_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - u0).count();
     char* d = (char*)c->meta_dev;
     auto at = [&](int i) { return (const void*)(d + c->meta_part_off[i]); };
     c->d_counts = (const DevCounts*)at(P_HDR);
@@ -728,7 +829,9 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         if (c->tree.root < 0) fail(TA_ERR_LOGIC, "no tree");
         cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
         // one decode step = plan + schedule + metadata upload, reused by every layer
-        plan_flatten(c->tree, bs, c->plan);
+        const auto t0 = std::chrono::steady_clock::now();
+        make_plan(c->tree, c->strategy, bs, c->plan);
+        const auto t1 = std::chrono::steady_clock::now();
         c->plan_valid = true;
         c->plan_version = c->tree.version;
         c->plan_bs = bs;
@@ -741,8 +844,10 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             fail(TA_ERR_INVALID_ARGUMENT, "prepare: GQA group size " + std::to_string(c->G) +
                                               " exceeds the FMA kernel's 16 rows (use bf16 KV with d_head 128)");
         build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, o, c->sched);
-        const Schedule& S = c->sched;
+        const auto t2 = std::chrono::steady_clock::now();
         upload_schedule(c, (cudaStream_t)stream);
+        c->t_plan_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+        c->t_sched_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count();
         c->prepared = true;
         c->prepared_version = c->tree.version;
         c->prepared_bs = bs;
@@ -911,6 +1016,9 @@ ta_status ta_io_stats_get(ta_ctx* c, ta_io_stats* o) {
                                   S.cta_pub_begin.size() + 2 * S.cta_pub.size() + S.cta_own_begin.size() +
                                   S.cta_own.size()) * 4;
         o->flops = S.masked_q_tokens * c->hq_loc * 4 * D;
+        o->host_plan_ns = c->t_plan_ns;
+        o->host_schedule_ns = c->t_sched_ns;
+        o->host_upload_ns = c->t_upload_ns;
     });
 }
 

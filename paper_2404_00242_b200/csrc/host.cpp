@@ -307,14 +307,17 @@ void PagePool::reset() {
 }
 
 // ===========================================================================
-// partition_flatten (partition.hpp:212-253) via leaf intervals.
+// The reference's partition strategies (partition.hpp:97-262) via leaf
+// intervals.  Leaves are in DFS order, so a node's queries
+// (queries_for_node, tree.hpp:169-178) are the contiguous leaf interval
+// [lo, hi) of its subtree, and every mask word is a contiguous run of bits.
 //
-// Walk nodes in DFS pre-order, stream their tokens, cut every block_size
-// tokens (0-token nodes contribute nothing).  Per flush the query list is the
-// union of the segments' leaf intervals in leaves() order; a segment's mask
-// bit j is set iff query j lies in the segment node's interval, i.e. a
-// contiguous run.  >64 queries: 64-query slices that keep every segment
-// (emit_groups, partition.hpp:102-126).  Bit-exact with plan_to_json.
+// Emitter::flush(segments) is emit_groups (partition.hpp:102-126) for one
+// chunk: the query list is the union of the segments' intervals in leaves()
+// order; > 64 queries give 64-query slices that keep every segment (even
+// with mask 0), else mask-0 segments are dropped; a group is emitted iff
+// some mask is set.  It also records the chunk view the device schedule is
+// built from.  Bit-exact with plan_to_json for every strategy.
 // ===========================================================================
 static inline uint64_t run_mask(int b, int e) {
     if (e <= b) return 0;
@@ -322,23 +325,36 @@ static inline uint64_t run_mask(int b, int e) {
     return (n >= 64 ? ~0ULL : ((1ULL << n) - 1)) << b;
 }
 
-void plan_flatten(const Tree& t, int bs, Plan& P) {
-    if (bs < 1) fail(TA_ERR_INVALID_ARGUMENT, "partition: block_size must be >= 1");
-    P = Plan{};
-    P.block_size = bs;
-    struct Pend {
-        int32_t node;
-        int64_t off, len;
-    };
-    std::vector<Pend> pend;
+namespace {
+
+struct Seg {
+    int32_t node;
+    int64_t off, len;
+};
+
+struct Emitter {
+    const Tree& t;
+    Plan& P;
     std::vector<std::pair<int32_t, int32_t>> iv;
     std::vector<int32_t> Q;
-    int64_t fill = 0;
 
-    auto flush = [&] {
-        if (pend.empty()) return;
+    void chunk_view(const std::vector<Seg>& segs) {
+        for (std::size_t s = 0; s < segs.size(); ++s) {
+            P.cseg_node.push_back(segs[s].node);
+            P.cseg_offset.push_back(segs[s].off);
+            P.cseg_len.push_back(segs[s].len);
+            P.cseg_lo.push_back(iv[s].first);
+            P.cseg_hi.push_back(iv[s].second);
+        }
+        P.chunk_seg_begin.push_back((int32_t)P.cseg_node.size());
+        P.chunk_q.insert(P.chunk_q.end(), Q.begin(), Q.end());
+        P.chunk_q_begin.push_back((int32_t)P.chunk_q.size());
+    }
+
+    void flush(const std::vector<Seg>& segs) {
+        if (segs.empty()) return;
         iv.clear();
-        for (const Pend& s : pend) iv.emplace_back(t.leaf_lo[s.node], t.leaf_hi[s.node]);
+        for (const Seg& s : segs) iv.emplace_back(t.leaf_lo[s.node], t.leaf_hi[s.node]);
         std::vector<std::pair<int32_t, int32_t>> sorted = iv;
         std::stable_sort(sorted.begin(), sorted.end());
         Q.clear();
@@ -348,17 +364,7 @@ void plan_flatten(const Tree& t, int bs, Plan& P) {
             for (int32_t q = from; q < hi; ++q) Q.push_back(q);
             end = std::max(end, hi);
         }
-        // chunk view
-        for (std::size_t s = 0; s < pend.size(); ++s) {
-            P.cseg_node.push_back(pend[s].node);
-            P.cseg_offset.push_back(pend[s].off);
-            P.cseg_len.push_back(pend[s].len);
-            P.cseg_lo.push_back(iv[s].first);
-            P.cseg_hi.push_back(iv[s].second);
-        }
-        P.chunk_seg_begin.push_back((int32_t)P.cseg_node.size());
-        P.chunk_q.insert(P.chunk_q.end(), Q.begin(), Q.end());
-        P.chunk_q_begin.push_back((int32_t)P.chunk_q.size());
+        chunk_view(segs);
         // reference groups
         const int nq = (int)Q.size();
         const bool split = nq > 64;
@@ -366,16 +372,16 @@ void plan_flatten(const Tree& t, int bs, Plan& P) {
             const int cnt = std::min(64, nq - base);
             const std::size_t seg_mark = P.seg_node.size();
             bool any = false;
-            for (std::size_t s = 0; s < pend.size(); ++s) {
+            for (std::size_t s = 0; s < segs.size(); ++s) {
                 const int b = (int)(std::lower_bound(Q.begin(), Q.end(), iv[s].first) - Q.begin());
                 const int e = (int)(std::lower_bound(Q.begin(), Q.end(), iv[s].second) - Q.begin());
                 const int bb = std::clamp(b, base, base + cnt) - base;
                 const int ee = std::clamp(e, base, base + cnt) - base;
                 const uint64_t mask = run_mask(bb, ee);
                 if (mask == 0 && !split) continue;
-                P.seg_node.push_back(pend[s].node);
-                P.seg_offset.push_back(pend[s].off);
-                P.seg_len.push_back(pend[s].len);
+                P.seg_node.push_back(segs[s].node);
+                P.seg_offset.push_back(segs[s].off);
+                P.seg_len.push_back(segs[s].len);
                 P.seg_mask.push_back(mask);
                 any = any || mask != 0;
             }
@@ -390,10 +396,21 @@ void plan_flatten(const Tree& t, int bs, Plan& P) {
             P.seg_begin.push_back((int32_t)P.seg_node.size());
             P.q_begin.push_back((int32_t)P.queries.size());
         }
-        pend.clear();
-        fill = 0;
-    };
+    }
+};
 
+}  // namespace
+
+// partition_flatten (partition.hpp:212-253): stream tokens in DFS pre-order,
+// skip 0-token nodes, flush every block_size tokens and at the end.
+void plan_flatten(const Tree& t, int bs, Plan& P) {
+    if (bs < 1) fail(TA_ERR_INVALID_ARGUMENT, "partition: block_size must be >= 1");
+    P = Plan{};
+    P.block_size = bs;
+    P.strategy = TA_STRATEGY_FLATTEN;
+    Emitter em{t, P, {}, {}};
+    std::vector<Seg> pend;
+    int64_t fill = 0;
     for (int32_t id : t.dfs) {
         int64_t remaining = t.count[id], offset = 0;
         while (remaining > 0) {
@@ -402,10 +419,99 @@ void plan_flatten(const Tree& t, int bs, Plan& P) {
             offset += take;
             remaining -= take;
             fill += take;
-            if (fill == bs) flush();
+            if (fill == bs) {
+                em.flush(pend);
+                pend.clear();
+                fill = 0;
+            }
         }
     }
-    flush();
+    em.flush(pend);
+}
+
+// partition_node (partition.hpp:176-187) / partition_node_chunk (:190-207):
+// one chunk per live node, or per block_size piece of it, with the node's
+// queries.
+static void plan_node(const Tree& t, int bs, bool chunked, Plan& P) {
+    if (chunked && bs < 1) fail(TA_ERR_INVALID_ARGUMENT, "partition: block_size must be >= 1");
+    P = Plan{};
+    P.block_size = chunked ? bs : 0;
+    P.strategy = chunked ? TA_STRATEGY_NODE_CHUNK : TA_STRATEGY_NODE;
+    Emitter em{t, P, {}, {}};
+    std::vector<Seg> one(1);
+    for (int32_t id : t.dfs) {
+        const int64_t n = t.count[id];
+        if (n == 0) continue;
+        const int64_t step = chunked ? bs : n;
+        for (int64_t off = 0; off < n; off += step) {
+            one[0] = {id, off, std::min<int64_t>(step, n - off)};
+            em.flush(one);
+        }
+    }
+}
+
+// partition_q_guided (partition.hpp:133-173): one group per leaf, its whole
+// root-to-leaf KV cut into blocks, every mask word 1 (shared prefixes are
+// loaded once per query: the redundancy the KV-guided strategies remove).
+static void plan_q_guided(const Tree& t, int bs, Plan& P) {
+    if (bs < 1) fail(TA_ERR_INVALID_ARGUMENT, "partition: block_size must be >= 1");
+    P = Plan{};
+    P.block_size = bs;
+    P.strategy = TA_STRATEGY_Q_GUIDED;
+    std::vector<int32_t> chain;
+    std::vector<Seg> segs;
+    for (int32_t li = 0; li < (int32_t)t.leaves.size(); ++li) {
+        const int32_t leaf = t.leaves[li];
+        chain.clear();
+        for (int32_t cur = leaf; cur != -1; cur = t.parent[cur]) chain.push_back(cur);
+        std::reverse(chain.begin(), chain.end());
+        int64_t fill = 0;
+        auto flush = [&] {
+            if (segs.empty()) return;
+            for (const Seg& s : segs) {
+                P.seg_node.push_back(s.node);
+                P.seg_offset.push_back(s.off);
+                P.seg_len.push_back(s.len);
+                P.seg_mask.push_back(1);
+                P.cseg_node.push_back(s.node);
+                P.cseg_offset.push_back(s.off);
+                P.cseg_len.push_back(s.len);
+                P.cseg_lo.push_back(li);
+                P.cseg_hi.push_back(li + 1);
+            }
+            P.queries.push_back(leaf);
+            P.seg_begin.push_back((int32_t)P.seg_node.size());
+            P.q_begin.push_back((int32_t)P.queries.size());
+            P.chunk_seg_begin.push_back((int32_t)P.cseg_node.size());
+            P.chunk_q.push_back(li);
+            P.chunk_q_begin.push_back((int32_t)P.chunk_q.size());
+            segs.clear();
+            fill = 0;
+        };
+        for (int32_t id : chain) {
+            int64_t remaining = t.count[id], offset = 0;
+            while (remaining > 0) {
+                const int64_t take = std::min<int64_t>(remaining, bs - fill);
+                segs.push_back({id, offset, take});
+                offset += take;
+                remaining -= take;
+                fill += take;
+                if (fill == bs) flush();
+            }
+        }
+        flush();
+    }
+}
+
+// make_plan (partition.hpp:255-262)
+void make_plan(const Tree& t, int strategy, int bs, Plan& P) {
+    switch (strategy) {
+        case TA_STRATEGY_Q_GUIDED: plan_q_guided(t, bs, P); return;
+        case TA_STRATEGY_NODE: plan_node(t, bs, false, P); return;
+        case TA_STRATEGY_NODE_CHUNK: plan_node(t, bs, true, P); return;
+        case TA_STRATEGY_FLATTEN: plan_flatten(t, bs, P); return;
+        default: fail(TA_ERR_INVALID_ARGUMENT, "unknown strategy " + std::to_string(strategy));
+    }
 }
 
 // plan_to_json(plan).dump() (serde.hpp:41-61): nlohmann objects are key-sorted
@@ -436,7 +542,10 @@ std::string plan_json(const Tree& t, const Plan& p) {
         }
         s += "]}";
     }
-    s += "],\"strategy\":\"flatten\"}";
+    static const char* names[] = {"q-guided", "node", "node-chunk", "flatten"};
+    s += "],\"strategy\":\"";
+    s += names[p.strategy];
+    s += "\"}";
     (void)t;
     return s;
 }
@@ -489,16 +598,15 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     if (S_max > 4095) fail(TA_ERR_INVALID_ARGUMENT, "schedule: too many slots per lane");
 
     // ---- 1. stripes
+    S.kv_tokens_unique = t.total_tokens();   // one pass over the tree's KV (ablation plans load more)
     std::vector<Stripe> stripes;
     std::vector<int32_t> tmp;
     for (int c = 0; c < nc; ++c) {
         const int qb = plan.chunk_q_begin[c], qe = plan.chunk_q_begin[c + 1];
         const int nq = qe - qb;
-        for (int s = plan.chunk_seg_begin[c]; s < plan.chunk_seg_begin[c + 1]; ++s)
-            S.kv_tokens_unique += plan.cseg_len[s];
         if (nq == 0) continue;
         const int32_t* q = plan.chunk_q.data() + qb;
-        Stripe* cur = stripes.empty() ? nullptr : &stripes.back();
+        Stripe* cur = stripes.empty() || !opt.fuse_chunks ? nullptr : &stripes.back();
         if (nq > S_max) {
             if (cur && cur->wide && (int)cur->qset.size() == nq && std::equal(q, q + nq, cur->qset.begin())) {
                 cur->c1 = c + 1;

@@ -102,6 +102,7 @@ struct PagePool : KvHook {
 // schedule is built from.
 struct Plan {
     int block_size = 128;
+    int strategy = 3;                          // TA_STRATEGY_* (partition.hpp:16): flatten by default
     // QkvGroups exactly as partition_flatten emits them
     std::vector<int32_t> seg_begin{0}, q_begin{0};
     std::vector<int32_t> seg_node, queries;
@@ -119,6 +120,7 @@ struct Plan {
 };
 
 void plan_flatten(const Tree& t, int block_size, Plan& out);   // partition.hpp:212-253
+void make_plan(const Tree& t, int strategy, int block_size, Plan& out);   // partition.hpp:255-262
 std::string plan_json(const Tree& t, const Plan& p);           // serde.hpp:41-61
 
 // ---------------------------------------------------------------------------
@@ -235,6 +237,8 @@ struct SchedOptions {
     int many_items = 4;
     int minmax = 1;            // CTA runs: 1 min-max budget (binary search; measured better on
                                // every config), 0 equal split points
+    bool fuse_chunks = true;   // stripes span consecutive plan chunks (flatten); the ablation
+                               // strategies run each plan group as its own stripe
     bool use_mma = true;       // bf16 d128 only
     int fma_max_rows = 8;      // rows per lane of the FMA kernel (8 or 16)
     bool final_direct = true;  // single-item leaf-heads written directly
