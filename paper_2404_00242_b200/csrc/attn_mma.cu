@@ -46,30 +46,50 @@ using namespace dev;
 
 constexpr int BM = 128;                                  // rows per item (TMEM lanes)
 constexpr int DH = 128;                                  // head dim
-constexpr int NSTAGE = 2;                                // KV ring depth
+#ifndef TA_NK
+#define TA_NK 2
+#endif
+#ifndef TA_NV
+#define TA_NV 2
+#endif
+constexpr int NK = TA_NK;                                // K ring depth (a K tile is released by its QK)
+constexpr int NV = TA_NV;                                // V ring depth (a V tile waits for the softmax and PV)
 constexpr int HALF = BM * 128;                           // one 64-column half of a [128][128] bf16 tile
 constexpr int TILE = 2 * HALF;                           // 32 KB
-constexpr int STAGE = 2 * TILE;                          // K + V
-constexpr int SMEM_KV = 0;                               // stage s: K at s*STAGE, V at +TILE
-constexpr int SMEM_BAR = NSTAGE * STAGE;                 // 196608
+constexpr int SMEM_K = 0;                                // K stage s at s * TILE
+constexpr int SMEM_V = NK * TILE;                        // V stage s at SMEM_V + s * TILE
+constexpr int SMEM_BAR = SMEM_V + NV * TILE;
 constexpr int SMEM_RED = SMEM_BAR + 256;                 // [2 parity][2 half][128] fp32 row max
 constexpr int SMEM_REDL = SMEM_RED + 2 * 2 * BM * 4;     // [2 half][128] fp32 row sum
-// the CTA's schedule, staged once before the dependency wait: items, their
-// tile offsets in the CTA's tile sequence, tile descriptors and metadata
-constexpr int MAXI = 32, MAXT = 112;
+// the CTA's schedule (ta_internal.h, namespace blob): header + per-item tile /
+// slot offsets, items, tile descriptors and metadata, slot leaves, and the
+// fused merge's owned records and publications, staged by bulk copies
+using blob::MAXI;
+using blob::MAXT;
+using blob::MAXS;
+using blob::MAXO;
+using blob::MAXP;
+using blob::HI;
+using blob::HT;
+using blob::HS;
 // epilogue staging: one row of O / l (this thread's 64 columns) per thread,
-// 256 B + 16 B pad (conflict-free 16-byte stores), written to global by one
-// bulk async copy per row
-constexpr int EPI_ROW = 272;
+// written to global by bulk async copies
+#ifndef TA_EPI_PASSES
+#define TA_EPI_PASSES 1
+#endif
+constexpr int EPI_PASSES = TA_EPI_PASSES;                // fp32 rows staged in 1 or 2 column passes
+constexpr int EPI_ROW = 256 / EPI_PASSES + 16;
 constexpr int SMEM_EPI = SMEM_REDL + 2 * BM * 4;        // [8 warps][32 rows][EPI_ROW]
-constexpr int SMEM_ITEM = SMEM_EPI + 8 * 32 * EPI_ROW;   // ItemDesc[MAXI]
-constexpr int SMEM_IOFF = SMEM_ITEM + MAXI * 32;         // int[MAXI + 1]
-constexpr int SMEM_TD = SMEM_IOFF + 256;                 // TileDesc[MAXT]
+constexpr int SMEM_HDR = SMEM_EPI + 8 * 32 * EPI_ROW;    // blob header + IOFF + SOFF (blob::H_ITEMS bytes)
+constexpr int SMEM_ITEM = SMEM_HDR + blob::H_ITEMS;      // ItemDesc[MAXI]
+constexpr int SMEM_TD = SMEM_ITEM + MAXI * 32;           // TileDesc[MAXT]
 constexpr int SMEM_TM = SMEM_TD + MAXT * 16;             // TileMeta[MAXT]
-constexpr int MAXS = 512;                                // staged slot leaves
-constexpr int SMEM_SOFF = SMEM_TM + MAXT * 64;           // int[MAXI + 1]: item -> offset into s_slot
-constexpr int SMEM_SLOT = SMEM_SOFF + 256;               // int[MAXS]
-constexpr int SMEM_BYTES = SMEM_SLOT + MAXS * 4 + 1024;  // + alignment slack
+constexpr int SMEM_SLOT = SMEM_TM + MAXT * 64;           // int[MAXS]
+constexpr int SMEM_OWN = SMEM_SLOT + MAXS * 4;           // int4[MAXO]
+constexpr int SMEM_OWNID = SMEM_OWN + MAXO * 16;         // int[MAXO]
+constexpr int SMEM_PUB = SMEM_OWNID + MAXO * 4;          // int2[MAXP]: (record, partials written here)
+constexpr int SMEM_BYTES = SMEM_PUB + MAXP * 8 + 1024;   // + alignment slack
+static_assert(SMEM_HDR % 16 == 0 && SMEM_ITEM % 16 == 0 && SMEM_SLOT % 16 == 0 && SMEM_OWN % 16 == 0, "bulk copy alignment");
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 constexpr int NTHREADS = 352;                           // 3 issuer warps + 8 softmax warps
 constexpr int SOFT0 = 3;                                 // first softmax warp
@@ -78,12 +98,37 @@ constexpr int NSOFT = 256;
 constexpr int TMEM_COLS = 512;
 constexpr int TMEM_S = 0, TMEM_O = 256, TMEM_Q = 384;   // S0, S1 (P aliased), O, Q0, Q1 (item parity)
 constexpr float kLazy = 8.0f;                            // rescale O only when the max grows by > 2^8
+// A/B ablations and the light CTA-phase trace (scripts/build_variant.sh,
+// scripts/light_spans.py); never defined in the product build
+#ifndef TA_ABL_STREAM
+#define TA_ABL_STREAM 0   // softmax warps release each tile without reading S (timing only)
+#endif
+#ifndef TA_ABL_NOEPI
+#define TA_ABL_NOEPI 0    // no epilogue stores (timing only)
+#endif
+#ifndef TA_LIGHT_TRACE
+#define TA_LIGHT_TRACE 0  // product kernel records CTA entry / items done / exit (globaltimer) into AttnArgs::trace
+#endif
+#define TA_LIGHT(slot, dep)                                                                        \
+    do {                                                                                           \
+        if constexpr (TA_LIGHT_TRACE && !TRACE) {                                                  \
+            if (a.trace) {                                                                         \
+                unsigned long long t_;                                                             \
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_) : "r"((unsigned)(dep)) : "memory"); \
+                a.trace[blockIdx.x * TRACE_SLOTS + (slot)] = (long long)t_;                        \
+            }                                                                                      \
+        }                                                                                          \
+    } while (0)
+#ifndef TA_ABL_NOPUB
+#define TA_ABL_NOPUB 0    // no fused merge (timing only)
+#endif
 
 // Per-tile barriers are double-buffered by tile parity (S_FULL, S_FREE,
 // P_FULL, O_FULL): the softmax warps may run one tile ahead of the PV
 // issuer, and a waiter must never be two phases behind its barrier.
-enum { FULLK = 0, FULLV = NSTAGE, EMPTYK = 2 * NSTAGE, EMPTYV = 3 * NSTAGE, S_FULL = 4 * NSTAGE, S_FREE = S_FULL + 2,
-       P_FULL = S_FULL + 4, O_FULL = S_FULL + 6, Q_FULL = S_FULL + 8, Q_FREE = S_FULL + 10, NBAR = S_FULL + 12 };
+enum { FULLK = 0, FULLV = NK, EMPTYK = NK + NV, EMPTYV = 2 * NK + NV, S_FULL = 2 * (NK + NV), S_FREE = S_FULL + 2,
+       P_FULL = S_FULL + 4, O_FULL = S_FULL + 6, Q_FULL = S_FULL + 8, Q_FREE = S_FULL + 10, META_HEAD = S_FULL + 12,
+       META_TAIL = S_FULL + 13, NBAR = S_FULL + 14 };
 constexpr int TMEM_SLOT = 240;                           // offset of the TMEM address in the barrier block
 static_assert(NBAR * 8 <= TMEM_SLOT, "barriers overlap the TMEM slot");
 
@@ -97,7 +142,7 @@ static_assert(NBAR * 8 <= TMEM_SLOT, "barriers overlap the TMEM slot");
 constexpr int TRACE_SLOTS = 256, TRACE_TILES = 27;   // tiles: slots 8..223
 __device__ __forceinline__ long long gtimer() {
     long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
     return t;
 }
 // epilogue phases ([0] O_FULL seen, [1] fenced, [4] l exchanged, [3] stores begin, [2]
@@ -112,6 +157,22 @@ __device__ __forceinline__ long long gtimer() {
             }                                                                                      \
         }                                                                                          \
     } while (0)
+// phase marks at slots 180..191 (debug): clock64 (cheap; a %globaltimer read
+// costs ~1 us and would distort the phases), max over the CTA's writers.  The
+// asm takes `dep` as an input so it cannot issue before that value exists (a
+// timer read right after a barrier is otherwise not ordered by it).  Slots
+// 192..195: globaltimer / clock64 at entry and at the end, to place each
+// CTA's clocks on the global timeline.
+#define TA_MARK(a, k, dep)                                                                          \
+    do {                                                                                           \
+        if constexpr (TRACE) {                                                                     \
+            if ((a).trace) {                                                                       \
+                unsigned long long _t;                                                             \
+                asm volatile("mov.u64 %0, %%clock64;" : "=l"(_t) : "r"((unsigned)(dep)) : "memory"); \
+                atomicMax(reinterpret_cast<unsigned long long*>((a).trace) + blockIdx.x * TRACE_SLOTS + (k), _t); \
+            }                                                                                      \
+        }                                                                                          \
+    } while (0)
 #define TA_TRACE(a, t, k)                                                                          \
     do {                                                                                           \
         if constexpr (TRACE) {                                                                     \
@@ -119,20 +180,28 @@ __device__ __forceinline__ long long gtimer() {
         }                                                                                          \
     } while (0)
 
-// ---- fused merge: the owner's wait for the published partial counts
+// ---- fused merge: the owner's wait for the published partial counts.  One
+// counter per 128-byte line: every waiting warp polls its line, and packed
+// counters turned a few L2 lines into hot spots that slowed the publications
+// themselves.
+#ifndef TA_POLL_NS
+#define TA_POLL_NS 256
+#endif
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 // Spin until `target` pieces are in.  A schedule bug must fail loudly, not
-// hang the GPU: trap after 2 s.
+// hang the GPU: trap after ~4e9 SM clocks (2 s at the boost clock).  The
+// timeout reads clock64 (cheap), never %globaltimer (slow to read: it
+// stretched every poll to ~1 us).
 __device__ __forceinline__ void wait_pieces(const unsigned* cnt, unsigned target) {
     if (ld_acquire(cnt) >= target) return;
-    const long long t0 = gtimer();
+    const long long t0 = clock64();
     while (ld_acquire(cnt) < target) {
-        __nanosleep(128);
-        if (gtimer() - t0 > 2000000000LL) __trap();
+        __nanosleep(TA_POLL_NS);
+        if (clock64() - t0 > 4000000000LL) __trap();
     }
 }
 
@@ -140,48 +209,6 @@ struct TmapSet {
     CUtensorMap k[4];   // boxes of 16, 32, 64, 128 pool rows x 64 columns
     CUtensorMap v[4];
 };
-
-// tree_reduce (attention.hpp:209-233) of 16 columns [16 chunk, +16) of one
-// merge record row (q head g): partials rec.z .. rec.z + rec.w - 1 in item
-// order, weights 2^(lse_p - max).  Loads of 4 partials in flight at a time.
-__device__ __forceinline__ void merge_chunk16(const AttnArgs& a, int4 rec, int g, int chunk) {
-    const int G = a.G;
-    float M = -INFINITY;
-    for (int p = 0; p < rec.w; ++p) M = fmaxf(M, __ldcg(a.part_lse + (size_t)(rec.z + p) * G + g));
-    float acc[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-    float den = 0.f;
-    for (int p0 = 0; p0 < rec.w; p0 += 4) {
-        float4 v[4][4];
-        float w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const bool ok = p0 + u < rec.w;
-            const size_t pid = (size_t)(rec.z + p0 + u);
-            w[u] = ok ? ex2(__ldcg(a.part_lse + pid * G + g) - M) : 0.f;
-            const float4* src = reinterpret_cast<const float4*>(a.part_o + (pid * G + g) * DH + 16 * chunk);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) v[u][i] = ok ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            den += w[u];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                acc[4 * i] = fmaf(w[u], v[u][i].x, acc[4 * i]);
-                acc[4 * i + 1] = fmaf(w[u], v[u][i].y, acc[4 * i + 1]);
-                acc[4 * i + 2] = fmaf(w[u], v[u][i].z, acc[4 * i + 2]);
-                acc[4 * i + 3] = fmaf(w[u], v[u][i].w, acc[4 * i + 3]);
-            }
-        }
-    }
-    const float inv = den > 0.f ? 1.f / den : 0.f;
-    const size_t ob = ((size_t)rec.x * a.hq_loc + (size_t)rec.y * G + g) * DH + 16 * chunk;
-    store_row<16>(a.out, ob, acc, inv, a.out_bf16);
-    if (chunk == 0 && a.lse)
-        a.lse[(size_t)rec.x * a.hq_loc + (size_t)rec.y * G + g] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
-}
 
 template <bool TRACE>
 __global__ void __launch_bounds__(NTHREADS, 1)
@@ -200,18 +227,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         timeline_mark(a.timeline, 4, true);
         timeline_mark(a.timeline, 4, false);
     }
-    const int it0 = a.cta_begin[blockIdx.x], it1 = a.cta_begin[blockIdx.x + 1];
-    const int n_items = it1 - it0;
+    if (TRACE && a.trace && threadIdx.x == 0) {
+        a.trace[blockIdx.x * TRACE_SLOTS + 192] = gtimer();
+        a.trace[blockIdx.x * TRACE_SLOTS + 193] = clock64();
+    }
+    if (threadIdx.x == 0) TA_MARK(a, 180, blockIdx.x);
+    if (TA_LIGHT_TRACE && !TRACE && a.trace && threadIdx.x == 0) a.trace[blockIdx.x * TRACE_SLOTS] = gtimer();
     ItemDesc* s_item = reinterpret_cast<ItemDesc*>(smem + SMEM_ITEM);
-    int* s_ioff = reinterpret_cast<int*>(smem + SMEM_IOFF);
     TileDesc* s_td = reinterpret_cast<TileDesc*>(smem + SMEM_TD);
     TileMeta* s_tm = reinterpret_cast<TileMeta*>(smem + SMEM_TM);
-    int* s_soff = reinterpret_cast<int*>(smem + SMEM_SOFF);
     int* s_slot = reinterpret_cast<int*>(smem + SMEM_SLOT);
+    int4* s_own = reinterpret_cast<int4*>(smem + SMEM_OWN);
+    int* s_own_id = reinterpret_cast<int*>(smem + SMEM_OWNID);
+    int2* s_pub = reinterpret_cast<int2*>(smem + SMEM_PUB);
+    const int32_t* s_hdr = reinterpret_cast<const int32_t*>(smem + SMEM_HDR);
+    const int* s_ioff = reinterpret_cast<const int*>(smem + SMEM_HDR + blob::IOFF);
+    const int* s_soff = reinterpret_cast<const int*>(smem + SMEM_HDR + blob::SOFF);
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2 * NSTAGE; ++i) mbar_init(BAR(FULLK + i), 1);       // FULLK, FULLV
-        for (int i = 0; i < 2 * NSTAGE; ++i) mbar_init(BAR(EMPTYK + i), 1);      // EMPTYK, EMPTYV
+        for (int i = 0; i < 2 * (NK + NV); ++i) mbar_init(BAR(FULLK + i), 1);   // FULLK, FULLV, EMPTYK, EMPTYV
         for (int i = 0; i < 2; ++i) {
             mbar_init(BAR(S_FULL + i), 1);
             mbar_init(BAR(S_FREE + i), 1);
@@ -222,8 +256,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(BAR(Q_FULL + i), NSOFT);
             mbar_init(BAR(Q_FREE + i), 1);
         }
+        mbar_init(BAR(META_HEAD), 1);
+        mbar_init(BAR(META_TAIL), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
+        // the schedule head: host-written before the launch, so read before the
+        // dependency wait; one round trip brings what the first tiles need
+        const uint8_t* hb = a.cta_heads + (size_t)blockIdx.x * blob::HEAD_BYTES;
+        mbar_expect_tx(BAR(META_HEAD), blob::HEAD_BYTES);
+        bulk_g2s(sbase + SMEM_HDR, hb, blob::H_ITEMS, BAR(META_HEAD));
+        bulk_g2s(sbase + SMEM_ITEM, hb + blob::H_ITEMS, HI * 32, BAR(META_HEAD));
+        bulk_g2s(sbase + SMEM_TD, hb + blob::H_TD, HT * 16, BAR(META_HEAD));
+        bulk_g2s(sbase + SMEM_TM, hb + blob::H_TM, HT * 64, BAR(META_HEAD));
+        bulk_g2s(sbase + SMEM_SLOT, hb + blob::H_SLOT, HS * 4, BAR(META_HEAD));
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -237,41 +282,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             prefetch_tmap(&tm.v[i]);
         }
     }
-    // stage this CTA's schedule (written by the host before the launch, so it
-    // is read before the dependency wait, overlapping the previous launch)
-    const int ni_s = min(n_items, MAXI);
-    for (int k = threadIdx.x; k < ni_s; k += NTHREADS) s_item[k] = a.items[it0 + k];
     tc_fence_before();
-    __syncthreads();
+    __syncthreads();   // barriers initialised, TMEM address written
     tc_fence_after();
+    mbar_wait(BAR(META_HEAD), 0);
+    const int n_items = s_hdr[blob::N_ITEMS], it0 = s_hdr[blob::IT0];
+    const int ni_s = min(n_items, MAXI);
+    const int nt_s = s_hdr[blob::N_TILES];   // staged tiles: CTA tile index < nt_s
+    const int ns_s = s_hdr[blob::N_SLOTS];   // staged slot leaves
     if (threadIdx.x == 0) {
-        int off = 0, soff = 0;
-        for (int k = 0; k < ni_s; ++k) {
-            s_ioff[k] = off;
-            off += s_item[k].tile_end - s_item[k].tile_begin;
-            s_soff[k] = soff;
-            soff += s_item[k].n_slots;
+        // the tail: everything past the head's items / tiles / slots, and the
+        // fused merge's lists (needed from tile HT / item HI / slot HS on)
+        const uint8_t* tb = a.cta_tails + s_hdr[blob::TAIL_OFF];
+        const uint32_t dst[7] = {sbase + SMEM_ITEM + HI * 32, sbase + SMEM_TD + HT * 16, sbase + SMEM_TM + HT * 64,
+                                 sbase + SMEM_SLOT + HS * 4,  sbase + SMEM_OWN,          sbase + SMEM_OWNID,
+                                 sbase + SMEM_PUB};
+        uint32_t tot = 0;
+        for (int i = 0; i < 7; ++i) tot += (uint32_t)s_hdr[blob::T_ITEMS + i];
+        mbar_expect_tx(BAR(META_TAIL), tot);
+        uint32_t off = 0;
+        for (int i = 0; i < 7; ++i) {
+            const uint32_t n = (uint32_t)s_hdr[blob::T_ITEMS + i];
+            if (n) bulk_g2s(dst[i], tb + off, n, BAR(META_TAIL));
+            off += n;
         }
-        s_ioff[ni_s] = off;
-        s_soff[ni_s] = soff;
     }
-    __syncthreads();
-    const int ns_s = min(s_soff[ni_s], MAXS);    // staged slot leaves
-    for (int x = threadIdx.x; x < ns_s; x += NTHREADS) {
-        int k = 0;
-        while (s_soff[k + 1] <= x) ++k;
-        s_slot[x] = a.slot_leaf[s_item[k].slot_begin + x - s_soff[k]];
-    }
-    const int nt_s = min(s_ioff[ni_s], MAXT);   // staged tiles: CTA tile index < nt_s
-    for (int x = threadIdx.x; x < nt_s; x += NTHREADS) {
-        int k = 0;
-        while (s_ioff[k + 1] <= x) ++k;
-        const int t = s_item[k].tile_begin + x - s_ioff[k];
-        s_td[x] = a.tiles[t];
-        s_tm[x] = a.tile_meta[t];
-    }
-    __syncthreads();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) TA_MARK(a, 181, tmem);
     if (TRACE && threadIdx.x == 0 && a.timeline) {   // debug: schedule staged
         timeline_mark(a.timeline, 6, true);
         timeline_mark(a.timeline, 6, false);
@@ -279,12 +316,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     pdl_launch_dependents();
     // warm L2 with the first tiles' KV and the first item's query rows while
     // the previous launch drains (prefetches carry no ordering obligations)
-    if (warp == 0 && lane < a.prefetch_tiles && lane < nt_s) {
+    if (warp == 0 && lane < a.prefetch_tiles && lane < min(nt_s, HT)) {
         int k = 0;
         while (s_ioff[k + 1] <= lane) ++k;
-        const int64_t row0 = a.layer_row0 + (int64_t)s_item[k].head * a.head_rows;
+        if (k >= HI) k = -1;   // its item is in the tail
+        const int64_t row0 = k < 0 ? 0 : a.layer_row0 + (int64_t)s_item[k].head * a.head_rows;
         const TileDesc td = s_td[lane];
-        for (int b = 0; b < td.nbox; ++b) {
+        for (int b = 0; b < (k < 0 ? 0 : td.nbox); ++b) {
             const int g = td.box[b] >> 2, sz = td.box[b] & 3;
             const int row = (int)(row0 + s_tm[lane].row[g]);
             tma_prefetch_2d(&tm.k[sz], 0, row);
@@ -312,16 +350,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         a.trace[blockIdx.x * TRACE_SLOTS + 2] = smid;
     }
     // schedule accessors: k = CTA-local item index, lt = CTA-local tile index
-    auto item_at = [&](int k) -> ItemDesc { return k < MAXI ? s_item[k] : a.items[it0 + k]; };
-    auto td_at = [&](int lt, int t) -> TileDesc { return lt < nt_s ? s_td[lt] : a.tiles[t]; };
-    auto tm_at = [&](int lt, int t) -> const TileMeta* { return lt < nt_s ? &s_tm[lt] : &a.tile_meta[t]; };
+    bool tail_in = false;   // this thread has seen the tail land
+    auto need_tail = [&]() {
+        if (!tail_in) {
+            mbar_wait(BAR(META_TAIL), 0);
+            tail_in = true;
+        }
+    };
+    auto item_at = [&](int k) -> ItemDesc {
+        if (k >= HI) need_tail();
+        return k < MAXI ? s_item[k] : a.items[it0 + k];
+    };
+    auto td_at = [&](int lt, int t) -> TileDesc {
+        if (lt >= HT) need_tail();
+        return lt < nt_s ? s_td[lt] : a.tiles[t];
+    };
+    auto tm_at = [&](int lt, int t) -> const TileMeta* {
+        if (lt >= HT) need_tail();
+        return lt < nt_s ? &s_tm[lt] : &a.tile_meta[t];
+    };
     auto leaf_at = [&](int k, const ItemDesc& I, int jj) -> int {   // leaf of slot jj of item k
-        return (k < ni_s && s_soff[k] + jj < ns_s) ? s_slot[s_soff[k] + jj] : a.slot_leaf[I.slot_begin + jj];
+        if (k < ni_s) {
+            const int x = s_soff[k] + jj;
+            if (x < ns_s) {
+                if (x >= HS) need_tail();
+                return s_slot[x];
+            }
+        }
+        return a.slot_leaf[I.slot_begin + jj];
     };
 
     if (warp == 0) {
         // ===================== TMA producer =====================
-        if (lane > 0) fill_empty(a, lane - 1, 31);
         if (lane == 0) {
             int gt = 0;
             for (int k = 0; k < n_items; ++k) {
@@ -330,10 +390,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
                     const TileDesc td = td_at(gt, t);
                     const TileMeta* tmp = tm_at(gt, t);
-                    const int s = gt % NSTAGE;
-                    const uint32_t ph = (uint32_t)(gt / NSTAGE) & 1u;
-                    const uint32_t kdst = sbase + SMEM_KV + (uint32_t)s * STAGE;
-                    const uint32_t vdst = kdst + TILE;
+                    const int s = gt % NK, sv = gt % NV;
+                    const uint32_t ph = (uint32_t)(gt / NK) & 1u, phv = (uint32_t)(gt / NV) & 1u;
+                    const uint32_t kdst = sbase + SMEM_K + (uint32_t)s * TILE;
+                    const uint32_t vdst = sbase + SMEM_V + (uint32_t)sv * TILE;
                     const uint32_t bytes = (uint32_t)td.ng * 4096u;
                     mbar_wait(BAR(EMPTYK + s), ph ^ 1);
                     mbar_expect_tx(BAR(FULLK + s), bytes);
@@ -344,13 +404,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         tma_load_2d(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s));
                     }
                     TA_TRACE(a, gt, 0);
-                    mbar_wait(BAR(EMPTYV + s), ph ^ 1);
-                    mbar_expect_tx(BAR(FULLV + s), bytes);
+                    if (gt == 0) TA_MARK(a, 183, bytes);
+                    if (gt == 0) TA_LIGHT(2, bytes);
+                    mbar_wait(BAR(EMPTYV + sv), phv ^ 1);
+                    mbar_expect_tx(BAR(FULLV + sv), bytes);
                     for (int b = 0; b < td.nbox; ++b) {
                         const int g = td.box[b] >> 2, sz = td.box[b] & 3;
                         const int row = (int)(row0 + tmp->row[g]);
-                        tma_load_2d(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + s));
-                        tma_load_2d(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + s));
+                        tma_load_2d(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + sv));
+                        tma_load_2d(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + sv));
                     }
                 }
             }
@@ -365,11 +427,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mbar_wait(BAR(Q_FULL + qb), (k >> 1) & 1);
                 for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
                     const int ng = td_at(gt, t).ng;
-                    const int s = gt % NSTAGE, sb = gt & 1;
-                    mbar_wait(BAR(FULLK + s), (uint32_t)(gt / NSTAGE) & 1u);
+                    const int s = gt % NK, sb = gt & 1;
+                    mbar_wait(BAR(FULLK + s), (uint32_t)(gt / NK) & 1u);
                     if (gt >= 2) mbar_wait(BAR(S_FREE + sb), ((gt >> 1) - 1) & 1);
                     tc_fence_after();
-                    const uint32_t sK = sbase + SMEM_KV + (uint32_t)s * STAGE;
+                    const uint32_t sK = sbase + SMEM_K + (uint32_t)s * TILE;
                     const uint32_t id = idesc_bf16(BM, 16 * ng, 0, 0);
 #pragma unroll
                     for (int kq = 0; kq < DH / 16; ++kq) {
@@ -391,12 +453,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const ItemDesc I = item_at(k);
                 for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
                     const int ng = td_at(gt, t).ng;
-                    const int s = gt % NSTAGE;
+                    const int s = gt % NV;
                     const int sb = gt & 1;
-                    mbar_wait(BAR(FULLV + s), (uint32_t)(gt / NSTAGE) & 1u);
+                    mbar_wait(BAR(FULLV + s), (uint32_t)(gt / NV) & 1u);
                     mbar_wait(BAR(P_FULL + sb), (gt >> 1) & 1);
                     tc_fence_after();
-                    const uint32_t sV = sbase + SMEM_KV + (uint32_t)s * STAGE + TILE;
+                    const uint32_t sV = sbase + SMEM_V + (uint32_t)s * TILE;
                     const uint32_t id = idesc_bf16(BM, DH, 0, 1);
                     const bool first = t == I.tile_begin;
                     // P of group kk: bf16 pairs in columns [16kk, 16kk+8) of S buffer sb
@@ -409,6 +471,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
         }
+        // leaf-heads with no path tokens (their outputs are not read in this
+        // launch): the idle lanes, after the PV issuer's loop
+        __syncwarp();
+        if (lane > 0) fill_empty(a, lane - 1, 31);
     } else {
         // ===================== softmax / epilogue (256 threads) =====================
         const int q4 = warp & 3;                 // TMEM lane quadrant of this warp (warps 3..10)
@@ -469,7 +535,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 nleaf = r < In.n_slots * G ? leaf_at(k + 1, In, r / G) : -1;
                 if (nleaf >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(q_row(In, nleaf)));
             }
-
             for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
                 const TileDesc td = td_at(gt, t);
                 const uint4 inf = *reinterpret_cast<const uint4*>(tm_at(gt, t)->info + 4 * h);
@@ -494,7 +559,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // S of my half into registers (one pass), tree mask, row max
                 uint32_t r0[16], r1[16], r2[16], r3[16];
                 float mx = -INFINITY;
-                if (warp_att) {
+                if (warp_att && !TA_ABL_STREAM) {
                     // groups past ng hold stale columns; lim == 0 masks them
                     TA_TMEM_LD16(s_addr + g0 * 16, r0);
                     TA_TMEM_LD16(s_addr + (g0 + 1) * 16, r1);
@@ -542,7 +607,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                 }
                 if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 5);
-                if (warp_att) {
+                if (warp_att && !TA_ABL_STREAM) {
                     // P = exp2(s * scale - m) -> bf16 pairs -> S columns [16g, 16g+8); l += sum(P)
                     const float negm = m == -INFINITY ? 0.f : -m;
                     float la = 0.f;
@@ -574,6 +639,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tc_fence_before();
                 mbar_arrive(BAR(P_FULL + sb));
                 if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 6);
+                if (threadIdx.x == TRACE_TID && gt == 0) TA_MARK(a, 184, __float_as_uint(l));
+                if (threadIdx.x == TRACE_TID && gt == 0) TA_LIGHT(3, __float_as_uint(l));
+                if (threadIdx.x == TRACE_TID && gt == 4) TA_LIGHT(7, __float_as_uint(l));
+                if (threadIdx.x == TRACE_TID && gt + 1 == s_ioff[ni_s]) TA_LIGHT(4, __float_as_uint(l));
+                if (threadIdx.x == TRACE_TID) TA_MARK(a, 185, __float_as_uint(l));
                 if (has_next && t == I.tile_begin) {
                     // next item's Q -> the other Q buffer (free once item k-1's QK is done)
                     uint4 qv[8];
@@ -592,6 +662,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             redl[h * BM + r] = l;
             named_bar(1 + q4, 64);
             l += redl[(h ^ 1) * BM + r];
+            if (threadIdx.x == TRACE_TID) TA_MARK(a, 186, __float_as_uint(l));
             TA_TRACE_EPI(a, k, 4);
             const float inv = l > 0.f ? 1.f / l : 0.f;
             const float lse2 = m + log2f(l);
@@ -602,7 +673,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     a.part_lse[(size_t)code * G + g_in] = lse2;
                 }
             }
-            if (warp_live) {
+            if (warp_live && !TA_ABL_NOEPI) {
                 // O / l -> this thread's staging row (its TMEM lane = output row,
                 // its 64 columns), then one bulk async copy of the row to the
                 // final output or the partial record: the stores drain in the
@@ -614,39 +685,49 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // the row's previous bulk copy (an earlier item) has read the staging
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 TA_TRACE_EPI(a, k, 3);
+                // fp32 rows go out in EPI_PASSES column passes through a staging
+                // row of 256 / EPI_PASSES bytes (the SMEM it saves deepens the V ring)
+                const int npass = st_bf16 ? 1 : EPI_PASSES;
+                const int cpp = 4 / npass;   // 16-column chunks per pass
+                char* dst = nullptr;
+                if (code != kSlotUnused)
+                    dst = code >= 0 ? reinterpret_cast<char*>(a.part_o + ((size_t)code * G + g_in) * DH + 64 * h)
+                                    : reinterpret_cast<char*>(a.out) +
+                                          (((size_t)(-1 - code) * a.hq_loc + I.head * G + g_in) * DH + 64 * h) * (a.out_bf16 ? 2 : 4);
 #pragma unroll 1
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t o[16];
-                    TA_TMEM_LD16(tmem + lane_addr + TMEM_O + h * 64 + c * 16, o);
-                    tmem_wait_ld();
-                    if constexpr (TRACE) {
-                        if (a.trace && threadIdx.x == TRACE_TID) a.trace[blockIdx.x * TRACE_SLOTS + 232 + c] = clock64();
-                    }
-                    float f[16];
+                for (int pass = 0; pass < npass; ++pass) {
+                    if (pass > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#pragma unroll 1
+                    for (int c = pass * cpp; c < (pass + 1) * cpp; ++c) {
+                        uint32_t o[16];
+                        TA_TMEM_LD16(tmem + lane_addr + TMEM_O + h * 64 + c * 16, o);
+                        tmem_wait_ld();
+                        float f[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(o[i]) * inv;
-                    if (st_bf16) {
-                        sts128(srow + (uint32_t)(c * 32), pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]),
-                               pack_bf16(f[6], f[7]));
-                        sts128(srow + (uint32_t)(c * 32 + 16), pack_bf16(f[8], f[9]), pack_bf16(f[10], f[11]),
-                               pack_bf16(f[12], f[13]), pack_bf16(f[14], f[15]));
-                    } else {
+                        for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(o[i]) * inv;
+                        if (st_bf16) {
+                            sts128(srow + (uint32_t)(c * 32), pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]),
+                                   pack_bf16(f[6], f[7]));
+                            sts128(srow + (uint32_t)(c * 32 + 16), pack_bf16(f[8], f[9]), pack_bf16(f[10], f[11]),
+                                   pack_bf16(f[12], f[13]), pack_bf16(f[14], f[15]));
+                        } else {
+                            const uint32_t o16 = (uint32_t)((c - pass * cpp) * 64);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            sts128(srow + (uint32_t)(c * 64 + 16 * q), __float_as_uint(f[4 * q]), __float_as_uint(f[4 * q + 1]),
-                                   __float_as_uint(f[4 * q + 2]), __float_as_uint(f[4 * q + 3]));
+                            for (int q = 0; q < 4; ++q)
+                                sts128(srow + o16 + 16 * q, __float_as_uint(f[4 * q]), __float_as_uint(f[4 * q + 1]),
+                                       __float_as_uint(f[4 * q + 2]), __float_as_uint(f[4 * q + 3]));
+                        }
                     }
-                }
-                if (code != kSlotUnused) {
-                    void* dst = code >= 0 ? static_cast<void*>(a.part_o + ((size_t)code * G + g_in) * DH + 64 * h)
-                                          : static_cast<void*>(reinterpret_cast<char*>(a.out) +
-                                                               (((size_t)(-1 - code) * a.hq_loc + I.head * G + g_in) * DH + 64 * h) *
-                                                                   (a.out_bf16 ? 2 : 4));
-                    fence_proxy_async();   // the staging writes -> visible to the bulk copy
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(srow),
-                                 "r"(st_bf16 ? 128u : 256u)
-                                 : "memory");
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    if (dst) {
+                        const uint32_t nb = st_bf16 ? 128u : 256u / npass;
+                        fence_proxy_async();   // the staging writes -> visible to the bulk copy
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + pass * nb), "r"(srow),
+                                     "r"(nb)
+                                     : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        TA_MARK(a, 187, srow);
+                        if (threadIdx.x == TRACE_TID && k + 1 == n_items) TA_LIGHT(5, srow);
+                    }
                 }
             }
             TA_TRACE_EPI(a, k, 2);
@@ -663,40 +744,68 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (warp >= SOFT0) {
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         if (a.fused_merge) asm volatile("fence.proxy.async.global;" ::: "memory");
+        TA_MARK(a, 188, lane);
+        if (threadIdx.x == TRACE_TID) TA_LIGHT(35, lane);
     }
     tc_fence_before();
     __syncthreads();
-    if (TRACE && a.trace && threadIdx.x == 0) a.trace[blockIdx.x * TRACE_SLOTS + 6] = gtimer();   // items done, copies landed
+    if (threadIdx.x == 0) TA_MARK(a, 196, s_ioff[0]);
+    if (threadIdx.x == 0) TA_LIGHT(36, s_ioff[0]);
+    if (TA_LIGHT_TRACE && !TRACE && a.trace && threadIdx.x == 0) {
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_) : "r"(s_ioff[0]) : "memory");
+        a.trace[blockIdx.x * TRACE_SLOTS + 6] = (long long)t_;
+    }
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
     }
-    if (a.fused_merge) {
+    if (a.fused_merge && !TA_ABL_NOPUB) {
+        need_tail();
+        // read here, not kept live across the item loop (register pressure)
+        const int n_own = s_hdr[blob::N_OWN], o0 = s_hdr[blob::O0];
+        const int n_pub = s_hdr[blob::N_PUB], pb0 = s_hdr[blob::PB0];
         // 1. publish: per record this CTA wrote partials for, one release-add
         //    of their count
-        const int p0 = a.cta_pub_begin[blockIdx.x], p1 = a.cta_pub_begin[blockIdx.x + 1];
-        for (int i = p0 + (int)threadIdx.x; i < p1; i += NTHREADS) {
-            const int2 pb = a.cta_pub[i];
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(a.merge_cnt + pb.x), "r"(pb.y) : "memory");
+        if ((int)threadIdx.x < n_pub) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if ((int)threadIdx.x < n_pub) TA_MARK(a, 197, n_pub);
+        if (threadIdx.x == 0) TA_LIGHT(37, n_pub);
+        for (int i = threadIdx.x; i < n_pub; i += NTHREADS) {
+            const int2 pb = i < MAXP ? s_pub[i] : a.cta_pub[pb0 + i];
+            asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(a.merge_cnt + (size_t)pb.x * kCntStride), "r"(pb.y) : "memory");
         }
-        // 2. merge the records this CTA owns, all threads: one thread per
-        //    (record, q head, 16-column chunk), tree_reduce in item order.
-        //    Every CTA has published before it waits here, so no wait can
-        //    block a publication.
-        const int o0 = a.cta_own_begin[blockIdx.x], o1 = a.cta_own_begin[blockIdx.x + 1];
+        if ((int)threadIdx.x < n_pub) TA_MARK(a, 189, n_pub);
+        if (threadIdx.x == 0) TA_LIGHT(9, n_pub);
+        // 2. merge the records this CTA owns: one warp per (record, q head),
+        //    tree_reduce in item order, every partial's loads in flight at
+        //    once (merge_record_row).  Every CTA has published before it waits
+        //    here, so no wait can block a publication.
         const int G = a.G;
-        for (int u = threadIdx.x; u < (o1 - o0) * G * 8; u += NTHREADS) {
-            const int mi = a.cta_own[o0 + u / (G * 8)];
-            const int g = (u / 8) % G, chunk = u % 8;
-            const int4 rec = __ldg(a.merge_rec + mi);
-            wait_pieces(a.merge_cnt + mi, (unsigned)rec.w);
-            merge_chunk16(a, rec, g, chunk);
+        for (int row = warp; row < n_own * G; row += NTHREADS / 32) {
+            const int k = row / G;
+            const int id = k < MAXO ? s_own_id[k] : a.cta_own[o0 + k];
+            const int4 rec = k < MAXO ? s_own[k] : __ldg(a.merge_rec + id);
+            if (lane == 0) wait_pieces(a.merge_cnt + (size_t)id * kCntStride, (unsigned)rec.w);
+            __syncwarp();
+            if (lane == 0) TA_MARK(a, 190, rec.w);
+            if (lane == 0) TA_LIGHT(12 + warp, rec.w);
+            merge_record_row<4>(a, rec, row % G, lane);
+            if (lane == 0) TA_LIGHT(24 + warp, rec.w);
         }
         __syncthreads();
         // the counters are ours alone now: reset them for the next launch
         // (which publishes only after its dependency wait, i.e. after this grid)
-        for (int i = o0 + (int)threadIdx.x; i < o1; i += NTHREADS) a.merge_cnt[a.cta_own[i]] = 0u;
+        for (int x = threadIdx.x; x < n_own; x += NTHREADS) a.merge_cnt[(size_t)(x < MAXO ? s_own_id[x] : a.cta_own[o0 + x]) * kCntStride] = 0u;
+    }
+    if (threadIdx.x == 0) TA_MARK(a, 191, *tmem_slot);
+    if (TA_LIGHT_TRACE && !TRACE && a.trace && threadIdx.x == 0) {
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_) : "r"(s_ioff[0]) : "memory");
+        a.trace[blockIdx.x * TRACE_SLOTS + 1] = (long long)t_;
+    }
+    if (TRACE && a.trace && threadIdx.x == 0) {
+        a.trace[blockIdx.x * TRACE_SLOTS + 195] = clock64();
+        a.trace[blockIdx.x * TRACE_SLOTS + 194] = gtimer();
     }
     if (TRACE && threadIdx.x == 0) timeline_mark(a.timeline, 0, false);
     if (TRACE && a.trace && threadIdx.x == 0) {
@@ -735,7 +844,7 @@ bool make_pool_tmap(void* tmap_out, const void* base, int64_t rows, int D, int b
 
 cudaError_t launch_attn_mma(const AttnArgs& a, bool pdl, cudaStream_t s) {
     if (!mma_supported(a.D, a.kv_bf16)) return cudaErrorNotSupported;
-    const bool trace = a.trace || a.timeline;
+    const bool trace = (a.trace && !TA_LIGHT_TRACE) || a.timeline;
     cudaError_t e = set_smem_attr_once(trace ? (const void*)attn_mma_kernel<true> : (const void*)attn_mma_kernel<false>,
                                        SMEM_BYTES);
     if (e != cudaSuccess) return e;

@@ -75,6 +75,8 @@ struct ta_ctx {
     const int2* d_cta_pub = nullptr;
     const int32_t* d_cta_own_begin = nullptr;
     const int32_t* d_cta_own = nullptr;
+    const uint8_t* d_cta_heads = nullptr;
+    const uint8_t* d_cta_tails = nullptr;
     unsigned* merge_cnt = nullptr;   // fused merge counters, one per merge record
     size_t merge_cnt_n = 0;          // capacity (records)
     bool fused_merge = true;         // option "fused_merge"
@@ -710,7 +712,7 @@ int fma_rows(int rows) { return rows <= 4 ? 4 : rows <= 8 ? 8 : 16; }
 // step never waits for the current step's upload.
 enum {
     P_HDR, P_TILES, P_TMETA, P_GROW, P_GINFO, P_ITEMS, P_CTAB, P_SLEAF, P_SOUT, P_MREC, P_PMERGE, P_PUBB, P_PUB,
-    P_EMPTY, P_OWNB, P_OWN, P_APPEND, NPART
+    P_EMPTY, P_OWNB, P_OWN, P_APPEND, P_HEADS, P_TAILS, NPART
 };
 
 static void upload_schedule(ta_ctx* c, cudaStream_t s) {
@@ -738,6 +740,8 @@ static void upload_schedule(ta_ctx* c, cudaStream_t s) {
         {S.cta_own_begin.data(), S.cta_own_begin.size() * 4},
         {S.cta_own.data(), S.cta_own.size() * 4},
         {c->pending_rows.data(), c->pending_rows.size() * 4},
+        {S.cta_heads.data(), S.cta_heads.size()},
+        {S.cta_tails.data(), S.cta_tails.size()},
     };
     static_assert(sizeof(src) / sizeof(src[0]) == NPART, "parts");
     // capacities (bytes): grow all exceeded parts by 1.5x, keep the rest
@@ -778,8 +782,8 @@ static void upload_schedule(ta_ctx* c, cudaStream_t s) {
             c->merge_cnt_n = std::max(n_rec * 3 / 2, c->merge_cnt_n);
             cudaFree(c->merge_cnt);
             c->merge_cnt = nullptr;
-            cuda_check(cudaMalloc(&c->merge_cnt, c->merge_cnt_n * sizeof(unsigned)), "cudaMalloc(merge counters)");
-            cuda_check(cudaMemsetAsync(c->merge_cnt, 0, c->merge_cnt_n * sizeof(unsigned), s), "cudaMemsetAsync");
+            cuda_check(cudaMalloc(&c->merge_cnt, c->merge_cnt_n * kCntStride * sizeof(unsigned)), "cudaMalloc(merge counters)");
+            cuda_check(cudaMemsetAsync(c->merge_cnt, 0, c->merge_cnt_n * kCntStride * sizeof(unsigned), s), "cudaMemsetAsync");
         }
         ++c->graph_epoch;
     }
@@ -816,6 +820,8 @@ static void upload_schedule(ta_ctx* c, cudaStream_t s) {
     c->d_cta_own_begin = (const int32_t*)at(P_OWNB);
     c->d_cta_own = (const int32_t*)at(P_OWN);
     c->d_append_rows = (const int32_t*)at(P_APPEND);
+    c->d_cta_heads = (const uint8_t*)at(P_HEADS);
+    c->d_cta_tails = (const uint8_t*)at(P_TAILS);
     c->n_append = (int64_t)c->pending_rows.size();
     c->pending_rows.clear();
     // The fused-merge counters are self-resetting; zero them only after a
@@ -844,6 +850,7 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             fail(TA_ERR_INVALID_ARGUMENT, "prepare: GQA group size " + std::to_string(c->G) +
                                               " exceeds the FMA kernel's 16 rows (use bf16 KV with d_head 128)");
         build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, o, c->sched);
+        if (o.use_mma) build_cta_blobs(c->sched);
         const auto t2 = std::chrono::steady_clock::now();
         upload_schedule(c, (cudaStream_t)stream);
         c->t_plan_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
@@ -891,6 +898,8 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.cta_own_begin = c->d_cta_own_begin;
     a.cta_own = c->d_cta_own;
     a.empty = c->d_empty;
+    a.cta_heads = c->d_cta_heads;
+    a.cta_tails = c->d_cta_tails;
     a.n_ctas = (int)S.cta_begin.size() - 1;
     a.G = c->G;
     a.hq_loc = c->hq_loc;

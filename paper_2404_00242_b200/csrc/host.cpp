@@ -929,7 +929,8 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     // them without an id list.
     std::vector<int32_t> rec((size_t)L * n_heads, -1);  // leaf-head -> merge record
     std::vector<int32_t> rec_n;                          // partials per record (counting sort)
-    for (const ItemDesc& it : S.items) {
+    for (int ii = 0; ii < (int)S.items.size(); ++ii) {
+        const ItemDesc& it = S.items[ii];
         for (int j = 0; j < it.n_slots; ++j) {
             int32_t& code = S.slot_out[it.out_begin + j];
             if (code == kSlotUnused) continue;
@@ -972,7 +973,6 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     for (ItemDesc& it : S.items)
         for (int j = 0; j < it.n_slots; ++j)
             if (S.slot_out[it.out_begin + j] >= 0) it.pad |= 1;   // holds partials: takes part in merges
-
     // Fused merge (tcgen05 kernel): no merge launch.  At its end, after all
     // its items, a CTA publishes the partials it wrote (per record: how many)
     // and only then merges the records it owns.  Publication never waits, so
@@ -1014,12 +1014,18 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
             }
         }
         std::vector<int32_t> own_n(n_cta + 1, 0);
-        for (int mi = 0; mi < nrec; ++mi) own_n[owner[mi] + 1]++;
+        int n_own_total = 0;
+        for (int mi = 0; mi < nrec; ++mi)
+            if (owner[mi] >= 0) {
+                own_n[owner[mi] + 1]++;
+                ++n_own_total;
+            }
         S.cta_own_begin.assign(n_cta + 1, 0);
         for (int c = 0; c < n_cta; ++c) S.cta_own_begin[c + 1] = S.cta_own_begin[c] + own_n[c + 1];
-        S.cta_own.resize(nrec);
+        S.cta_own.resize(n_own_total);
         std::vector<int32_t> pos(S.cta_own_begin.begin(), S.cta_own_begin.end() - 1);
-        for (int mi = 0; mi < nrec; ++mi) S.cta_own[pos[owner[mi]]++] = mi;
+        for (int mi = 0; mi < nrec; ++mi)
+            if (owner[mi] >= 0) S.cta_own[pos[owner[mi]]++] = mi;
     }
     for (int32_t l = 0; l < L; ++l)
         for (int h = 0; h < n_heads; ++h)
@@ -1028,6 +1034,98 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
                 S.empty.push_back(h);
             }
     for (int32_t l : t.leaves) S.masked_q_tokens += t.path_tokens(l);
+}
+
+// Per-CTA schedule blobs (ta_internal.h, namespace blob): the tcgen05
+// kernel's SMEM staging laid out on the host, so a CTA's first round trip
+// (one fixed-size head copy) brings everything it needs to start streaming.
+void build_cta_blobs(Schedule& S) {
+    using namespace blob;
+    const int n_cta = (int)S.cta_begin.size() - 1;
+    S.cta_heads.assign((size_t)std::max(n_cta, 1) * HEAD_BYTES, 0);
+    S.cta_tails.clear();
+    auto put = [](std::vector<uint8_t>& v, const void* p, size_t n) {
+        const uint8_t* b = static_cast<const uint8_t*>(p);
+        v.insert(v.end(), b, b + n);
+    };
+    auto pad16 = [](std::vector<uint8_t>& v) { v.resize((v.size() + 15) & ~size_t(15), 0); };
+    std::vector<int32_t> slots;
+    std::vector<TileDesc> tds;
+    std::vector<TileMeta> tms;
+    for (int c = 0; c < n_cta; ++c) {
+        uint8_t* head = S.cta_heads.data() + (size_t)c * HEAD_BYTES;
+        int32_t* hdr = reinterpret_cast<int32_t*>(head + HDR);
+        int32_t* ioff = reinterpret_cast<int32_t*>(head + IOFF);
+        int32_t* soff = reinterpret_cast<int32_t*>(head + SOFF);
+        const int it0 = S.cta_begin[c], ni = S.cta_begin[c + 1] - it0;
+        const int ni_s = std::min(ni, MAXI);
+        tds.clear();
+        tms.clear();
+        slots.clear();
+        int off = 0, so = 0;
+        for (int k = 0; k < ni_s; ++k) {
+            const ItemDesc& it = S.items[it0 + k];
+            ioff[k] = off;
+            soff[k] = so;
+            off += it.tile_end - it.tile_begin;
+            so += it.n_slots;
+            for (int t = it.tile_begin; t < it.tile_end && (int)tds.size() < MAXT; ++t) {
+                tds.push_back(S.tiles[t]);
+                tms.push_back(S.tile_meta[t]);
+            }
+            for (int j = 0; j < it.n_slots && (int)slots.size() < MAXS; ++j) slots.push_back(S.slot_leaf[it.slot_begin + j]);
+        }
+        ioff[ni_s] = off;
+        soff[ni_s] = so;
+        const int nt_s = (int)tds.size(), ns_s = (int)slots.size();
+        int n_own = 0, n_pub = 0, o0 = 0, pb0 = 0;
+        if (S.fused_merge) {
+            o0 = S.cta_own_begin[c];
+            n_own = S.cta_own_begin[c + 1] - o0;
+            pb0 = S.cta_pub_begin[c];
+            n_pub = S.cta_pub_begin[c + 1] - pb0;
+        }
+        hdr[N_ITEMS] = ni;
+        hdr[N_TILES] = nt_s;
+        hdr[N_SLOTS] = ns_s;
+        hdr[N_OWN] = n_own;
+        hdr[N_PUB] = n_pub;
+        hdr[IT0] = it0;
+        hdr[O0] = o0;
+        hdr[PB0] = pb0;
+        std::memcpy(head + H_ITEMS, S.items.data() + it0, (size_t)std::min(ni_s, HI) * sizeof(ItemDesc));
+        std::memcpy(head + H_TD, tds.data(), (size_t)std::min(nt_s, HT) * sizeof(TileDesc));
+        std::memcpy(head + H_TM, tms.data(), (size_t)std::min(nt_s, HT) * sizeof(TileMeta));
+        std::memcpy(head + H_SLOT, slots.data(), (size_t)std::min(ns_s, HS) * 4);
+        // tail sections
+        hdr[TAIL_OFF] = (int32_t)S.cta_tails.size();
+        size_t b0 = S.cta_tails.size();
+        if (ni_s > HI) put(S.cta_tails, S.items.data() + it0 + HI, (size_t)(ni_s - HI) * sizeof(ItemDesc));
+        hdr[T_ITEMS] = (int32_t)(S.cta_tails.size() - b0);
+        b0 = S.cta_tails.size();
+        if (nt_s > HT) put(S.cta_tails, tds.data() + HT, (size_t)(nt_s - HT) * sizeof(TileDesc));
+        hdr[T_TD] = (int32_t)(S.cta_tails.size() - b0);
+        b0 = S.cta_tails.size();
+        if (nt_s > HT) put(S.cta_tails, tms.data() + HT, (size_t)(nt_s - HT) * sizeof(TileMeta));
+        hdr[T_TM] = (int32_t)(S.cta_tails.size() - b0);
+        b0 = S.cta_tails.size();
+        if (ns_s > HS) put(S.cta_tails, slots.data() + HS, (size_t)(ns_s - HS) * 4);
+        pad16(S.cta_tails);
+        hdr[T_SLOT] = (int32_t)(S.cta_tails.size() - b0);
+        b0 = S.cta_tails.size();
+        const int no_s = std::min(n_own, MAXO), np_s = std::min(n_pub, MAXP);
+        for (int x = 0; x < no_s; ++x) put(S.cta_tails, &S.merge_rec[S.cta_own[o0 + x]], 16);
+        hdr[T_OWN] = (int32_t)(S.cta_tails.size() - b0);
+        b0 = S.cta_tails.size();
+        if (no_s) put(S.cta_tails, S.cta_own.data() + o0, (size_t)no_s * 4);
+        pad16(S.cta_tails);
+        hdr[T_OWNID] = (int32_t)(S.cta_tails.size() - b0);
+        b0 = S.cta_tails.size();
+        if (np_s) put(S.cta_tails, S.cta_pub.data() + pb0, (size_t)np_s * 8);
+        pad16(S.cta_tails);
+        hdr[T_PUB] = (int32_t)(S.cta_tails.size() - b0);
+    }
+    if (S.cta_tails.empty()) S.cta_tails.resize(16, 0);
 }
 
 }  // namespace ta

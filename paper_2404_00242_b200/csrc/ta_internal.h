@@ -173,6 +173,28 @@ static_assert(sizeof(ItemDesc) == 32, "ItemDesc layout");
 
 constexpr int32_t kSlotUnused = INT32_MIN;   // slot_out: slot not attended in this item
 
+// Per-CTA schedule blob of the tcgen05 kernel, built on the host in the
+// kernel's SMEM layout so a CTA stages its schedule with bulk copies: a
+// fixed-size head (one copy round trip, enough to start streaming) and a
+// variable tail (issued once the head has landed; read from tile HT, item HI,
+// slot HS on).  Entries past the SMEM capacities are read from the global
+// schedule arrays.
+namespace blob {
+constexpr int MAXI = 32, MAXT = 112, MAXS = 512, MAXO = 32, MAXP = 64;   // SMEM capacities
+constexpr int HI = 2, HT = 4, HS = 128;                                  // head part
+enum { N_ITEMS, N_TILES, N_SLOTS, N_OWN, N_PUB, IT0, TAIL_OFF, O0, PB0, T_ITEMS, T_TD, T_TM, T_SLOT, T_OWN, T_OWNID,
+       T_PUB, NHDR };
+constexpr int HDR = 0;                        // int32[NHDR]: counts are staged counts except N_ITEMS / N_OWN / N_PUB
+constexpr int IOFF = 64;                      // int32[MAXI + 1]: CTA-local first tile of each staged item
+constexpr int SOFF = IOFF + 144;              // int32[MAXI + 1]: CTA-local first slot of each staged item
+constexpr int H_ITEMS = SOFF + 144;           // ItemDesc[HI]
+constexpr int H_TD = H_ITEMS + HI * 32;       // TileDesc[HT]
+constexpr int H_TM = H_TD + HT * 16;          // TileMeta[HT]
+constexpr int H_SLOT = H_TM + HT * 64;        // int32[HS]
+constexpr int HEAD_BYTES = H_SLOT + HS * 4;   // tail: items, tiles, metas, slots, own records, own ids, pubs (16-byte sections)
+static_assert(NHDR * 4 <= IOFF && (MAXI + 1) * 4 <= 144 && HEAD_BYTES % 16 == 0 && H_ITEMS % 16 == 0, "blob layout");
+}  // namespace blob
+
 inline uint32_t grp_pack(int count, int b, int e) {
     return (uint32_t)count | ((uint32_t)b << 8) | ((uint32_t)e << 20);
 }
@@ -204,6 +226,8 @@ struct Schedule {
     std::vector<Pub> cta_pub;
     std::vector<int32_t> cta_own_begin;   // [n_ctas + 1] into cta_own
     std::vector<int32_t> cta_own;         // merge records
+    std::vector<uint8_t> cta_heads;   // [n_ctas][blob::HEAD_BYTES]
+    std::vector<uint8_t> cta_tails;   // packed tails (16-byte sections)
     std::vector<int32_t> empty;       // [n][2] (leaf, local head) pairs with no path tokens
     int32_t n_lanes = 0;
     int32_t max_lane_rows = 0;        // max rows (slots x G) of any lane
@@ -220,6 +244,7 @@ struct Schedule {
         merge_begin.clear(); merge_parts.clear(); merge_rec.clear(); empty.clear();
         fused_merge = false;
         cta_pub_begin.clear(); cta_pub.clear(); cta_own_begin.clear(); cta_own.clear();
+        cta_heads.clear(); cta_tails.clear();
         n_lanes = n_partials = n_leaves = max_lane_rows = 0;
         kv_tokens_unique = kv_rows_loaded = masked_q_tokens = n_stripes = 0;
     }
@@ -250,5 +275,7 @@ struct SchedOptions {
 
 void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int group_size,
                     int n_kv_heads_local, const SchedOptions& opt, Schedule& out);
+// per-CTA head / tail blobs of a built schedule (tcgen05 kernel)
+void build_cta_blobs(Schedule& S);
 
 }  // namespace ta

@@ -22,6 +22,9 @@ struct DevCounts {
 };
 static_assert(sizeof(DevCounts) == 256, "DevCounts layout");
 
+// fused-merge counters: one per merge record, kCntStride words apart (own L2 line)
+constexpr int kCntStride = 32;
+
 struct AttnArgs {
     // KV pools of this layer.  FMA path: element pointers + per-head stride.
     const void* k;
@@ -58,6 +61,8 @@ struct AttnArgs {
     const int32_t* cta_own_begin;   // [n_ctas + 1] into cta_own
     const int32_t* cta_own;         // records the CTA merges
     const int32_t* empty;     // [n_empty][2] (leaf, head)
+    const uint8_t* cta_heads; // tcgen05 kernel: per-CTA schedule blobs (ta_internal.h, namespace blob)
+    const uint8_t* cta_tails;
     int n_ctas;
     int G;
     int hq_loc;

@@ -16,3 +16,6 @@ for c in ${CFGS:-few_shot}; do
     python -c "import json; d=json.loads(open('gpurun_out/bench_$c.log').read().strip().splitlines()[-1]); print('$c [$o]', round(d['value'],1), 'us/step', round(d['us_per_layer'],2), 'us/layer frac', round(d['roofline']['frac'],3), d['roofline']['bound'], 'launches', d['gpu_launches'], d['schedule'])" 2>/dev/null || tail -5 gpurun_out/bench_$c.log
   done
 done
+for c in ${PHASES}; do
+  timeout 300 python scripts/trace_marks.py $c $OPTS > gpurun_out/marks_$c.txt 2>&1; cat gpurun_out/marks_$c.txt
+done

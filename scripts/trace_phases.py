@@ -48,8 +48,8 @@ for rep in range(6):
         torch.cuda.synchronize()
         t = tr.cpu().numpy().reshape(n_cta, 256)
         t0 = t[:, 0].min()
-        res.append(((t[:, 0] - t0) / 1e3, (t[:, 6] - t0) / 1e3, (t[:, 1] - t0) / 1e3))
-st, it, en = (np.stack([r[i] for r in res[NL:]]) for i in range(3))
+        res.append(((t[:, 0] - t0) / 1e3, (t[:, 6] - t0) / 1e3, (t[:, 1] - t0) / 1e3, np.where(t[:, 7] > 0, (t[:, 7] - t0) / 1e3, np.nan), np.where(t[:, 236] > 0, (t[:, 236] - t0) / 1e3, np.nan), np.where(t[:, 237] > 0, (t[:, 237] - t0) / 1e3, np.nan), np.where(t[:, 200:211] > 0, (t[:, 200:211] - t0) / 1e3, np.nan), np.where(t[:, 238] > 0, (t[:, 238] - t0) / 1e3, np.nan), np.where(t[:, 239] > 0, (t[:, 239] - t0) / 1e3, np.nan)))
+st, it, en, wd, md, pu, fw, fe, pf = (np.stack([r[i] for r in res[NL:]]) for i in range(9))
 pc = lambda a: " ".join(f"{x:6.2f}" for x in np.percentile(a, [0, 10, 50, 90, 100]))
 print(f"{name} {' '.join(opts)}: {n_cta} CTAs, {len(res) - NL} isolated launches; percentiles 0/10/50/90/100 (us from first CTA start)")
 print("  CTA start     ", pc(st))
@@ -57,3 +57,18 @@ print("  items done    ", pc(it))
 print("  CTA end       ", pc(en))
 print("  merge phase   ", pc(en - it))
 print("  span (max end) mean %.2f" % en.max(axis=1).mean())
+pn = lambda a: " ".join(f"{x:6.2f}" for x in np.nanpercentile(a, [0, 10, 50, 90, 100]))
+last = it.max(axis=1, keepdims=True)
+print("  waits done - last items done  ", pn(wd - last))
+print("  merge loop end - last items   ", pn(md - last))
+print("  CTA end - last items done     ", pn(en - last))
+print("  publish - own items done      ", pn(pu - it))
+print("  pre-fence - own items done    ", pn(pf - it))
+print("  pre-fence (abs)               ", pn(pf))
+lastpf = np.nanmax(pf, axis=1, keepdims=True)
+print("  CTA end - last pre-fence      ", pn(en - lastpf))
+print("  first wait - last pre-fence   ", pn(fw - lastpf[..., None]))
+print("  fence done - pre-fence        ", pn(fe - pf))
+print("  publish - last items done     ", pn(pu - last))
+print("  first wait done - last items  ", pn(fw - last[..., None]))
+print("  first wait done - own publish ", pn(fw - pu[..., None]))
