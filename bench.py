@@ -553,6 +553,60 @@ def measure_decode_loop(name, cfg, args, world, rank, local_rank):
     return res
 
 
+# ------------------------------------------------------- prefix split (§8e)
+def measure_prefix_split(name, cfg, args, world, rank, local_rank):
+    """The optional cross-GPU split of the flattened tree (SURVEY §8e,
+    paper_2404_00242_b200/prefix_split.py): every rank attends ALL kv heads
+    over 1/world of the flattened tokens, then one NCCL all-to-all by head
+    slice and ta_lse_merge.  Per-step device time (max over ranks) beside the
+    head-sharded step of the same config."""
+    import torch
+    import torch.distributed as dist
+    from paper_2404_00242_b200.prefix_split import PrefixSplitAttention
+    snap = build_snapshot(cfg)
+    root, ids, par, cnt = snap
+    h_kv, h_q, d, L_layers = cfg["h_kv"], cfg["h_q"], cfg["d"], cfg["n_layers"]
+    pages = int(sum((int(c) + 15) // 16 for c in cnt)) // world + len(ids) + 16
+    ps = PrefixSplitAttention(snap, rank, world, n_layers=L_layers, n_q_heads=h_q, n_kv_heads=h_kv, d_head=d,
+                              kv_dtype=cfg["dtype"], max_pages=pages, device=local_rank)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    for layer in range(L_layers):
+        for i, n in enumerate(ids):
+            off, cn = (int(x) for x in ps.ranges[i])
+            if cn:   # this rank's slice of the node's KV (values do not change the work)
+                ps.ctx.write_kv(layer, int(n), (torch.rand((cn, h_kv, d), generator=gen, device="cuda") * 2 - 1).bfloat16(),
+                                (torch.rand((cn, h_kv, d), generator=gen, device="cuda") * 2 - 1).bfloat16())
+    L = len(ps.ctx.leaves())
+    q = (torch.rand((L_layers, L, h_q, d), generator=gen, device="cuda") * 2 - 1).bfloat16()
+    out = torch.empty((L_layers, L, h_q // world, d), dtype=torch.bfloat16, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ps.ctx.prepare(128, stream)
+        for layer in range(L_layers):
+            ps.attend(layer, q[layer], out[layer], stream=stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    K = min(args.steps, 10)
+    e0.record(stream)
+    for _ in range(K):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / K], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    io = ps.ctx.io_stats()
+    return {"us_per_step": float(t.item()) * 1e3, "tokens_per_rank": int(sum(int(c) for _, c in ps.ranges)),
+            "exchange_bytes_per_layer_per_rank": L * h_q * (d + 1) * 4 * (world - 1) // world,
+            "kv_bytes_per_layer_per_rank": io.kv_bytes,
+            "path": "per layer: ta_attend over this rank's token range (all heads, fp32 partials + lse), "
+                    "NCCL all_to_all_single by head slice, ta_lse_merge -> this rank's heads (bf16)"}
+
+
 # ---------------------------------------------------------- trace replay
 # Paper Table 10 (end-to-end KV IO, TB, DeFT-Flatten; Llama-3-8B counted as 32
 # heads, io_model.hpp:144-146) and Table 8 (attention latency, s, A100 80GB),
@@ -690,6 +744,9 @@ def main():
     ap.add_argument("--replay", default=None,
                     help="comma-separated reference presets to replay end to end (or 'all'); prints one JSON line")
     ap.add_argument("--no-replay", action="store_true", help="skip the trace replays in the default run")
+    ap.add_argument("--prefix-split", action="store_true",
+                    help="also time the cross-GPU split of the flattened tree (all heads per rank, NCCL all-to-all "
+                         "+ LSE merge) for the config; needs torchrun (N >= 1)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
@@ -708,7 +765,7 @@ def main():
         names = REPLAY_PRESETS if args.replay == "all" else args.replay.split(",")
         print(json.dumps({"trace_replay": {n: replay_trace(n, args, local_rank) for n in names}}))
         return
-    if world > 1:
+    if world > 1 or (args.prefix_split and "RANK" in os.environ):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
@@ -728,6 +785,12 @@ def main():
                                      steps=min(args.steps, 20))
             except Exception as e:   # a sub-config must never sink the headline line
                 subs[name] = {"error": str(e)[:300]}
+    split = None
+    if args.prefix_split and torch.distributed.is_initialized():
+        try:
+            split = measure_prefix_split(args.config, cfg, args, world, rank, local_rank)
+        except Exception as e:
+            split = {"error": str(e)[:300]}
     replays = {}
     if world == 1 and not args.headline_only and not args.no_replay and args.config == "few_shot":
         for name in REPLAY_PRESETS:
@@ -736,7 +799,7 @@ def main():
             except Exception as e:
                 replays[name] = {"error": str(e)[:300]}
     if rank != 0:
-        if world > 1:
+        if torch.distributed.is_initialized():
             torch.distributed.destroy_process_group()
         return
     line = {
@@ -770,8 +833,10 @@ def main():
         line["configs"] = subs
     if replays:
         line["trace_replay"] = replays
+    if split:
+        line["prefix_split"] = split
     print(json.dumps(line))
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 
 

@@ -205,6 +205,17 @@ ta_status ta_attend_host_async(ta_ctx* ctx, int layer, const void* q_host, void*
                                void* stream);
 ta_status ta_attend_host_wait(ta_ctx* ctx);
 
+/* Cross-GPU prefix split: merge n_parts partial results of the
+ * same rows -- each the attention of a row over a disjoint token range, as
+ * ta_attend returns it (out fp32 normalised, lse natural log, -inf for a row
+ * with no tokens in that range) -- into the attention over the union:
+ * tree_reduce (attention.hpp:209-233) in part order.  part_o [n_parts][rows][d]
+ * fp32, part_lse [n_parts][rows]; out [rows][d] (out_bf16: bf16 else fp32),
+ * lse_out [rows] (optional).  Device pointers, 16-byte aligned; d % 4 == 0,
+ * n_parts <= 32.  No context needed (device = the current one). */
+ta_status ta_lse_merge(const float* part_o, const float* part_lse, int n_parts, int64_t rows, int d, void* out,
+                       int out_bf16, float* lse_out, void* stream);
+
 typedef struct ta_io_stats {
     int64_t n_chunks;          /* flatten chunks (sibling groups fused) */
     int64_t n_groups;          /* reference QkvGroups */

@@ -1072,6 +1072,18 @@ ta_status ta_schedule_get(ta_ctx* c, int bs, ta_schedule_view* o) {
     });
 }
 
+ta_status ta_lse_merge(const float* part_o, const float* part_lse, int n_parts, int64_t rows, int d, void* out,
+                       int out_bf16, float* lse_out, void* stream) {
+    return guard([&] {
+        if (!part_o || !part_lse || !out) fail(TA_ERR_INVALID_ARGUMENT, "lse_merge: null pointer");
+        if (n_parts < 1 || n_parts > 32) fail(TA_ERR_INVALID_ARGUMENT, "lse_merge: n_parts must be in [1, 32]");
+        if (rows < 0 || d < 1) fail(TA_ERR_INVALID_ARGUMENT, "lse_merge: bad rows / d");
+        if (((uintptr_t)part_o | (uintptr_t)out) & 15) fail(TA_ERR_INVALID_ARGUMENT, "lse_merge: pointers must be 16-byte aligned");
+        cuda_check(launch_lse_merge(part_o, part_lse, n_parts, rows, d, out, out_bf16, lse_out, (cudaStream_t)stream),
+                   "lse_merge");
+    });
+}
+
 int ta_launches_per_attend(ta_ctx* c) {
     if (!c || !c->prepared) return 0;
     return c->sched.fused_merge ? 1 : 2;

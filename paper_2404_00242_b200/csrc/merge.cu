@@ -37,7 +37,57 @@ __global__ void __launch_bounds__(128, 8) merge_kernel(const AttnArgs a) {
     if (threadIdx.x == 0) timeline_mark(a.timeline, 2, false);
 }
 
+// ta_lse_merge: one warp per row; lane k < n holds part k's lse, every lane
+// DPL columns of each part (all parts' loads in flight), combined in part order.
+template <int DPL>
+__global__ void __launch_bounds__(256) lse_merge_kernel(const float* __restrict__ part_o, const float* __restrict__ part_lse,
+                                                        int n_parts, int64_t rows, int d, void* out, int out_bf16,
+                                                        float* lse_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const float lp = lane < n_parts ? part_lse[(int64_t)lane * rows + row] : -INFINITY;
+    float M = lp;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    const float w = (lp == -INFINITY) ? 0.f : __expf(lp - M);
+    float den = w;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
+    for (int c0 = lane * DPL; c0 < d; c0 += 32 * DPL) {
+        float acc[DPL];
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
+        for (int p = 0; p < n_parts; ++p) {
+            const float wp = __shfl_sync(0xffffffffu, w, p);
+            float v[DPL];
+            ldcg_cols<DPL>(part_o + ((int64_t)p * rows + row) * d + c0, v);
+#pragma unroll
+            for (int i = 0; i < DPL; ++i) acc[i] = fmaf(wp, v[i], acc[i]);
+        }
+        const float inv = den > 0.f ? 1.f / den : 0.f;
+        if (out_bf16) {
+#pragma unroll
+            for (int i = 0; i < DPL; ++i)
+                reinterpret_cast<__nv_bfloat16*>(out)[row * d + c0 + i] = __float2bfloat16_rn(acc[i] * inv);
+        } else {
+#pragma unroll
+            for (int i = 0; i < DPL; ++i) reinterpret_cast<float*>(out)[row * d + c0 + i] = acc[i] * inv;
+        }
+    }
+    if (lane == 0 && lse_out) lse_out[row] = M == -INFINITY ? -INFINITY : M + logf(den);
+}
+
 }  // namespace
+
+cudaError_t launch_lse_merge(const float* part_o, const float* part_lse, int n_parts, int64_t rows, int d, void* out,
+                             int out_bf16, float* lse_out, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((rows + 7) / 8);
+    if (d % 4 == 0) lse_merge_kernel<4><<<grid, 256, 0, s>>>(part_o, part_lse, n_parts, rows, d, out, out_bf16, lse_out);
+    else lse_merge_kernel<1><<<grid, 256, 0, s>>>(part_o, part_lse, n_parts, rows, d, out, out_bf16, lse_out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_merge(const AttnArgs& a, int n_sms, bool pdl, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};

@@ -92,6 +92,9 @@ int fma_tile_groups(int D, int esize);
 // split-K merge of the partial records (after the attention launch); a fixed
 // grid of 4 x n_sms CTAs loops over counts->n_merge records (graph-stable)
 cudaError_t launch_merge(const AttnArgs& a, int n_sms, bool pdl, cudaStream_t s);
+// ta_lse_merge: n_parts partial results of the same rows -> their merge (prefix split)
+cudaError_t launch_lse_merge(const float* part_o, const float* part_lse, int n_parts, int64_t rows, int d, void* out,
+                             int out_bf16, float* lse_out, cudaStream_t s);
 // ta_kv_append: src rows [n][n_loc][D] -> pool rows rows[i] for every local
 // head, n = counts->n_append read on the device (graph-stable, fixed grid)
 cudaError_t launch_kv_append(const void* src_k, const void* src_v, void* dst_k, void* dst_v, const int32_t* rows,
