@@ -767,12 +767,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int n_pub = s_hdr[blob::N_PUB], pb0 = s_hdr[blob::PB0];
         // 1. publish: per record this CTA wrote partials for, one release-add
         //    of their count
-        if ((int)threadIdx.x < n_pub) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#ifndef TA_PUB
+#define TA_PUB 0   // A/B: 0 fence.acq_rel + relaxed red, 1 red.release, 2 no ordering (timing only)
+#endif
+        if (TA_PUB == 0 && (int)threadIdx.x < n_pub) asm volatile("fence.acq_rel.gpu;" ::: "memory");
         if ((int)threadIdx.x < n_pub) TA_MARK(a, 197, n_pub);
         if (threadIdx.x == 0) TA_LIGHT(37, n_pub);
         for (int i = threadIdx.x; i < n_pub; i += NTHREADS) {
             const int2 pb = i < MAXP ? s_pub[i] : a.cta_pub[pb0 + i];
-            asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(a.merge_cnt + (size_t)pb.x * kCntStride), "r"(pb.y) : "memory");
+            if (TA_PUB == 1)
+                asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.merge_cnt + (size_t)pb.x * kCntStride), "r"(pb.y) : "memory");
+            else
+                asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(a.merge_cnt + (size_t)pb.x * kCntStride), "r"(pb.y) : "memory");
         }
         if ((int)threadIdx.x < n_pub) TA_MARK(a, 189, n_pub);
         if (threadIdx.x == 0) TA_LIGHT(9, n_pub);
@@ -781,16 +787,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         //    once (merge_record_row).  Every CTA has published before it waits
         //    here, so no wait can block a publication.
         const int G = a.G;
-        for (int row = warp; row < n_own * G; row += NTHREADS / 32) {
-            const int k = row / G;
+        // two rows per warp (half-warp merges): every owned row in one round
+        const int hw = lane >> 4;
+        for (int row0 = 2 * warp; row0 < n_own * G; row0 += 2 * (NTHREADS / 32)) {
+            const int row = row0 + hw;
+            const bool active = row < n_own * G;
+            const int k = active ? row / G : 0;
             const int id = k < MAXO ? s_own_id[k] : a.cta_own[o0 + k];
             const int4 rec = k < MAXO ? s_own[k] : __ldg(a.merge_rec + id);
-            if (lane == 0) wait_pieces(a.merge_cnt + (size_t)id * kCntStride, (unsigned)rec.w);
+            if (active && (lane & 15) == 0) wait_pieces(a.merge_cnt + (size_t)id * kCntStride, (unsigned)rec.w);
             __syncwarp();
             if (lane == 0) TA_MARK(a, 190, rec.w);
-            if (lane == 0) TA_LIGHT(12 + warp, rec.w);
-            merge_record_row<4>(a, rec, row % G, lane);
-            if (lane == 0) TA_LIGHT(24 + warp, rec.w);
+            merge_record_row_half(a, rec, row % G, lane & 15, active);
         }
         __syncthreads();
         // the counters are ours alone now: reset them for the next launch

@@ -262,6 +262,86 @@ __device__ __forceinline__ void merge_record_row(const AttnArgs& a, int4 rec, in
     if (lane == 0 && a.lse) a.lse[(size_t)rec.x * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
 }
 
+// Half-warp variant for D = 128: lanes [16 hw, 16 hw + 16) merge one row, 8
+// columns per lane, so a warp merges two rows at once; up to 16 partials' lse
+// (lane k: partial k) and 8 partials' columns in flight per round trip.
+__device__ __forceinline__ void merge_record_row_half(const AttnArgs& a, int4 rec, int g, int lane16, bool active) {
+    constexpr int PB = 8;
+    const int G = a.G;
+    const int hq = rec.y * G + g;
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    float M = -INFINITY, den = 0.f;
+    const int n = active ? rec.w : 0;
+    const int nmax = max(n, __shfl_xor_sync(0xffffffffu, n, 16));   // the warp's two rows: one trip count
+    for (int base = 0; base < nmax; base += 16) {
+        const int np = max(0, min(16, n - base));
+        const int p0 = rec.z + base;
+        const float lp = lane16 < np ? __ldcg(a.part_lse + (size_t)(p0 + lane16) * G + g) : -INFINITY;
+        float4 v[PB][2];
+#pragma unroll
+        for (int u = 0; u < PB; ++u) {
+            if (u < np) {
+                const float4* src = reinterpret_cast<const float4*>(a.part_o + ((size_t)(p0 + u) * G + g) * 128 + lane16 * 8);
+                v[u][0] = __ldcg(src);
+                v[u][1] = __ldcg(src + 1);
+            } else {
+                v[u][0] = v[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        float bm = lp;
+#pragma unroll
+        for (int off = 8; off > 0; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, off));
+        const float nm = fmaxf(M, bm);
+        const float rescale = (M == -INFINITY || nm == -INFINITY) ? 0.f : ex2(M - nm);
+        if (nm != -INFINITY) {
+            den *= rescale;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] *= rescale;
+            M = nm;
+        }
+        const float w = (lp == -INFINITY || M == -INFINITY) ? 0.f : ex2(lp - M);
+        float ws = w;
+#pragma unroll
+        for (int off = 8; off > 0; off >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, off);
+        den += ws;
+        for (int p = 0; p < 16; p += PB) {
+            if (p > 0) {
+#pragma unroll
+                for (int u = 0; u < PB; ++u) {
+                    if (p + u < np) {
+                        const float4* src =
+                            reinterpret_cast<const float4*>(a.part_o + ((size_t)(p0 + p + u) * G + g) * 128 + lane16 * 8);
+                        v[u][0] = __ldcg(src);
+                        v[u][1] = __ldcg(src + 1);
+                    } else {
+                        v[u][0] = v[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < PB; ++u) {
+                const float wu = __shfl_sync(0xffffffffu, w, (threadIdx.x & 16) + ((p + u) & 15));
+                const float ww = p + u < np ? wu : 0.f;
+                acc[0] = fmaf(ww, v[u][0].x, acc[0]);
+                acc[1] = fmaf(ww, v[u][0].y, acc[1]);
+                acc[2] = fmaf(ww, v[u][0].z, acc[2]);
+                acc[3] = fmaf(ww, v[u][0].w, acc[3]);
+                acc[4] = fmaf(ww, v[u][1].x, acc[4]);
+                acc[5] = fmaf(ww, v[u][1].y, acc[5]);
+                acc[6] = fmaf(ww, v[u][1].z, acc[6]);
+                acc[7] = fmaf(ww, v[u][1].w, acc[7]);
+            }
+        }
+    }
+    if (!active) return;
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    const size_t ob = ((size_t)rec.x * a.hq_loc + hq) * 128 + lane16 * 8;
+    store_row<8>(a.out, ob, acc, inv, a.out_bf16);
+    if (lane16 == 0 && a.lse) a.lse[(size_t)rec.x * a.hq_loc + hq] = M == -INFINITY ? -INFINITY : (M + log2f(den)) * kLn2;
+}
+
 // Leaf-heads whose path holds no tokens: out = 0, lse = -inf (they are
 // absent from the reference's AttentionOutput).  `nl` lanes (ids 0..nl-1) of
 // one warp, strided over CTAs.
