@@ -372,6 +372,26 @@ def measure(name, cfg, args, world, rank, local_rank, clocks=None, with_cpu=Fals
     torch.cuda.synchronize()
     attend_ms = ev0.elapsed_time(ev1) / (reps * L_layers)
 
+    # ---- the same layer calls WITHOUT programmatic dependent launch: each
+    # attention launch starts only after the previous one has completed, as
+    # in a model where o_proj / MLP kernels run between the layers' attention
+    # calls (no prologue / tail overlap between consecutive attention launches)
+    no_overlap_ms = None
+    if graph is not None:
+        ctx.set_option("pdl", 0)
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            layers()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(reps):
+            g2.replay()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        no_overlap_ms = ev0.elapsed_time(ev1) / (reps * L_layers)
+        ctx.set_option("pdl", 1)
+        del g2
+
     # ---- e2e through the public host-buffer entry (H2D q + D2H out per layer)
     e2e = None
     if not args.no_e2e:
@@ -437,7 +457,11 @@ def measure(name, cfg, args, world, rank, local_rank, clocks=None, with_cpu=Fals
                      "traffic": profile_traffic(name), "alg_bytes_per_launch": alg_bytes,
                      "alg_flops_per_launch": io.flops, "intensity_flop_per_byte": io.flops / max(1, alg_bytes),
                      "other": tensor_line if not tensor_bound else hbm_line})
-    res = {"value": ms * 1000.0, "ms_per_step": ms, "us_per_layer": attend_ms * 1000.0, "roofline": roofline,
+    if no_overlap_ms:   # the same fraction when consecutive attention launches do not overlap
+        roofline["frac_no_launch_overlap"] = roofline["frac"] * attend_ms / no_overlap_ms
+    res = {"value": ms * 1000.0, "ms_per_step": ms, "us_per_layer": attend_ms * 1000.0,
+           "us_per_layer_no_launch_overlap": no_overlap_ms * 1000.0 if no_overlap_ms else None,
+           "roofline": roofline,
            "e2e": e2e, "kv_io_bytes_per_step": io.kv_bytes * L_layers,
            "kv_bytes_loaded_per_step": io.kv_bytes_loaded * L_layers,
            "partial_io_bytes_per_step": io.partial_bytes * L_layers, "meta_bytes_per_step": io.meta_bytes,
@@ -820,6 +844,7 @@ def main():
         "partial_io_bytes_per_step": head["partial_io_bytes_per_step"],
         "meta_bytes_per_step": head["meta_bytes_per_step"],
         "us_per_layer": head["us_per_layer"],
+        "us_per_layer_no_launch_overlap": head.get("us_per_layer_no_launch_overlap"),
         "roofline": head["roofline"],
         "cpu_baseline": head.get("cpu_baseline"),
         "e2e": head["e2e"],
