@@ -187,7 +187,14 @@ ta_status ta_io_analytical(ta_ctx* ctx, int algorithm, const ta_cost_params* par
  * out [n_leaves][n_local_q_heads][d_head] in out_dtype;
  * lse (optional, may be NULL) [n_leaves][n_local_q_heads] fp32, natural log.
  * Leaves whose path holds no tokens get lse = -inf and out = 0 (they are
- * absent from the reference's AttentionOutput map). */
+ * absent from the reference's AttentionOutput map).
+ * Ordering: ta_attend waits for the previous kernel on `stream` before it
+ * reads q or writes out / lse (programmatic dependent launch).  KV pools are
+ * written only by ta_kv_write (synchronous) and ta_kv_append (rows known at
+ * ta_prepare), so with option "early_kv" = 1 a CTA starts loading its
+ * leading KV tiles -- those no pending ta_kv_append row touches -- before
+ * that wait (off by default; a caller that writes the pools by other means
+ * on the same stream must leave it off). */
 ta_status ta_prepare(ta_ctx* ctx, int block_size, void* stream);
 ta_status ta_attend(ta_ctx* ctx, int layer, const void* q, void* out, float* lse, void* stream);
 /* End-to-end variant over HOST buffers (pinned or pageable): H2D q, attend,

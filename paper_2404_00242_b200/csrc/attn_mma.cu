@@ -285,7 +285,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_before();
     __syncthreads();   // barriers initialised, TMEM address written
     tc_fence_after();
+    if (threadIdx.x == 0) TA_LIGHT(38, *tmem_slot);   // barriers initialised, TMEM allocated
     mbar_wait(BAR(META_HEAD), 0);
+    if (threadIdx.x == 0) TA_LIGHT(39, s_hdr[0]);      // schedule head landed
     const int n_items = s_hdr[blob::N_ITEMS], it0 = s_hdr[blob::IT0];
     const int ni_s = min(n_items, MAXI);
     const int nt_s = s_hdr[blob::N_TILES];   // staged tiles: CTA tile index < nt_s
@@ -315,20 +317,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     pdl_launch_dependents();
     // warm L2 with the first tiles' KV and the first item's query rows while
-    // the previous launch drains (prefetches carry no ordering obligations)
-    if (warp == 0 && lane < a.prefetch_tiles && lane < min(nt_s, HT)) {
+    // the previous launch drains (prefetches carry no ordering obligations).
+    // Issued by the PV issuer's lanes, idle until the first P: from the
+    // producer's thread they delayed its own first loads by ~1.5 µs.  Tiles
+    // the producer loads before the wait (n_early) need none.
+    if (warp == 2 && lane < a.prefetch_tiles && lane < min(nt_s, HT) && lane >= (a.early_kv ? s_hdr[blob::N_EARLY] : 0)) {
         int k = 0;
         while (s_ioff[k + 1] <= lane) ++k;
-        if (k >= HI) k = -1;   // its item is in the tail
-        const int64_t row0 = k < 0 ? 0 : a.layer_row0 + (int64_t)s_item[k].head * a.head_rows;
-        const TileDesc td = s_td[lane];
-        for (int b = 0; b < (k < 0 ? 0 : td.nbox); ++b) {
-            const int g = td.box[b] >> 2, sz = td.box[b] & 3;
-            const int row = (int)(row0 + s_tm[lane].row[g]);
-            tma_prefetch_2d(&tm.k[sz], 0, row);
-            tma_prefetch_2d(&tm.k[sz], 64, row);
-            tma_prefetch_2d(&tm.v[sz], 0, row);
-            tma_prefetch_2d(&tm.v[sz], 64, row);
+        if (k < HI) {   // else its item is in the tail
+            const int64_t row0 = a.layer_row0 + (int64_t)s_item[k].head * a.head_rows;
+            const TileDesc td = s_td[lane];
+            for (int b = 0; b < td.nbox; ++b) {
+                const int g = td.box[b] >> 2, sz = td.box[b] & 3;
+                const int row = (int)(row0 + s_tm[lane].row[g]);
+                tma_prefetch_2d(&tm.k[sz], 0, row);
+                tma_prefetch_2d(&tm.k[sz], 64, row);
+                tma_prefetch_2d(&tm.v[sz], 0, row);
+                tma_prefetch_2d(&tm.v[sz], 64, row);
+            }
         }
     }
     if (warp >= SOFT0 && n_items > 0) {
@@ -340,7 +346,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(qp));
         }
     }
-    pdl_wait();   // previous launch finished: queries, outputs, partial scratch are ours
+    // previous launch finished: queries, outputs, partial scratch are ours.  The
+    // producer waits inside its loop, after loading the leading tiles no
+    // pending ta_kv_append row touches (KV is written only by ta_kv_write,
+    // synchronous, or ta_kv_append, whose rows the host knows)
+    const int n_early = a.early_kv ? s_hdr[blob::N_EARLY] : 0;
+    if (!(warp == 0 && lane == 0)) pdl_wait();
+    if (threadIdx.x == 0) TA_LIGHT(40, s_hdr[1]);
     if (TRACE && threadIdx.x == 0) timeline_mark(a.timeline, 0, true);
     if (TRACE && a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS] = gtimer();
@@ -388,6 +400,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const ItemDesc I = item_at(k);
                 const int64_t row0 = a.layer_row0 + (int64_t)I.head * a.head_rows;
                 for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
+                    if (gt == n_early) pdl_wait();
                     const TileDesc td = td_at(gt, t);
                     const TileMeta* tmp = tm_at(gt, t);
                     const int s = gt % NK, sv = gt % NV;

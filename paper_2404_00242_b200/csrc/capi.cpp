@@ -4,6 +4,7 @@
 // fallback for attention.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -60,6 +61,10 @@ struct ta_ctx {
     int64_t n_append = 0;         // tokens whose rows the last ta_prepare uploaded for ta_kv_append
     int64_t t_plan_ns = 0, t_sched_ns = 0, t_upload_ns = 0;   // host time of the last ta_prepare
     std::vector<int32_t> pending_rows;   // pool rows of tokens appended since the last ta_prepare
+    std::vector<int32_t> pending_sorted; // (sorted copy for the schedule blobs)
+    bool early_kv = false;               // option "early_kv": leading KV tiles loaded before the dependency wait
+                                         // (off: in the 32-layer graph it measured +0.9 µs per few-shot layer,
+                                         // the early loads competing with the previous launch's merge phase)
     const TileDesc* d_tiles = nullptr;
     const TileMeta* d_tile_meta = nullptr;
     const int32_t* d_grp_row = nullptr;
@@ -323,6 +328,8 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->timeline = v;
         } else if (k == "trace_ptr") {
             c->trace = v;
+        } else if (k == "early_kv") {
+            c->early_kv = v != 0;
         } else if (k == "fused_merge") {
             c->fused_merge = v != 0;
         } else if (k == "strategy") {
@@ -334,7 +341,7 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             fail(TA_ERR_INVALID_ARGUMENT, "unknown option " + k);
         }
         // launch-only knobs keep the prepared schedule
-        if (k != "trace_ptr" && k != "timeline_ptr" && k != "pdl" && k != "prefetch_tiles")
+        if (k != "trace_ptr" && k != "timeline_ptr" && k != "pdl" && k != "prefetch_tiles" && k != "early_kv")
             c->prepared = false;
     });
 }
@@ -850,7 +857,11 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             fail(TA_ERR_INVALID_ARGUMENT, "prepare: GQA group size " + std::to_string(c->G) +
                                               " exceeds the FMA kernel's 16 rows (use bf16 KV with d_head 128)");
         build_schedule(c->tree, c->pool, c->plan, c->G, c->shape.n_local_kv_heads, o, c->sched);
-        if (o.use_mma) build_cta_blobs(c->sched);
+        if (o.use_mma) {
+            c->pending_sorted.assign(c->pending_rows.begin(), c->pending_rows.end());
+            std::sort(c->pending_sorted.begin(), c->pending_sorted.end());
+            build_cta_blobs(c->sched, c->pending_sorted);
+        }
         const auto t2 = std::chrono::steady_clock::now();
         upload_schedule(c, (cudaStream_t)stream);
         c->t_plan_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
@@ -910,6 +921,7 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.trace = reinterpret_cast<long long*>(c->trace);
     a.timeline = reinterpret_cast<unsigned long long*>(c->timeline);
     a.prefetch_tiles = c->prefetch_tiles;
+    a.early_kv = c->early_kv ? 1 : 0;
 
     const SchedOptions o = effective_opts(c);
     // both kernels move q / out / lse rows in 16-byte units

@@ -1039,7 +1039,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
 // Per-CTA schedule blobs (ta_internal.h, namespace blob): the tcgen05
 // kernel's SMEM staging laid out on the host, so a CTA's first round trip
 // (one fixed-size head copy) brings everything it needs to start streaming.
-void build_cta_blobs(Schedule& S) {
+void build_cta_blobs(Schedule& S, const std::vector<int32_t>& pending_rows) {
     using namespace blob;
     const int n_cta = (int)S.cta_begin.size() - 1;
     S.cta_heads.assign((size_t)std::max(n_cta, 1) * HEAD_BYTES, 0);
@@ -1093,6 +1093,19 @@ void build_cta_blobs(Schedule& S) {
         hdr[IT0] = it0;
         hdr[O0] = o0;
         hdr[PB0] = pb0;
+        // leading tiles (<= 2: the ring) free of rows the step's ta_kv_append
+        // writes: the kernel may load them before its dependency wait
+        int early = 0;
+        for (; early < std::min(nt_s, 2); ++early) {
+            bool hit = false;
+            for (int g = 0; g < tds[early].ng && !hit; ++g) {
+                const int32_t r0 = tms[early].row[g], r1 = r0 + (int32_t)(tms[early].info[g] & 0xffu);
+                auto it = std::lower_bound(pending_rows.begin(), pending_rows.end(), r0);
+                hit = it != pending_rows.end() && *it < r1;
+            }
+            if (hit) break;
+        }
+        hdr[N_EARLY] = early;
         std::memcpy(head + H_ITEMS, S.items.data() + it0, (size_t)std::min(ni_s, HI) * sizeof(ItemDesc));
         std::memcpy(head + H_TD, tds.data(), (size_t)std::min(nt_s, HT) * sizeof(TileDesc));
         std::memcpy(head + H_TM, tms.data(), (size_t)std::min(nt_s, HT) * sizeof(TileMeta));

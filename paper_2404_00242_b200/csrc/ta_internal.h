@@ -183,9 +183,9 @@ namespace blob {
 constexpr int MAXI = 32, MAXT = 112, MAXS = 512, MAXO = 32, MAXP = 64;   // SMEM capacities
 constexpr int HI = 2, HT = 4, HS = 128;                                  // head part
 enum { N_ITEMS, N_TILES, N_SLOTS, N_OWN, N_PUB, IT0, TAIL_OFF, O0, PB0, T_ITEMS, T_TD, T_TM, T_SLOT, T_OWN, T_OWNID,
-       T_PUB, NHDR };
+       T_PUB, N_EARLY, NHDR };
 constexpr int HDR = 0;                        // int32[NHDR]: counts are staged counts except N_ITEMS / N_OWN / N_PUB
-constexpr int IOFF = 64;                      // int32[MAXI + 1]: CTA-local first tile of each staged item
+constexpr int IOFF = 80;                      // int32[MAXI + 1]: CTA-local first tile of each staged item
 constexpr int SOFF = IOFF + 144;              // int32[MAXI + 1]: CTA-local first slot of each staged item
 constexpr int H_ITEMS = SOFF + 144;           // ItemDesc[HI]
 constexpr int H_TD = H_ITEMS + HI * 32;       // TileDesc[HT]
@@ -276,6 +276,8 @@ struct SchedOptions {
 void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int group_size,
                     int n_kv_heads_local, const SchedOptions& opt, Schedule& out);
 // per-CTA head / tail blobs of a built schedule (tcgen05 kernel)
-void build_cta_blobs(Schedule& S);
+// pending_rows: pool rows the step's ta_kv_append writes (sorted); a CTA's
+// leading tiles without any of them may be loaded before the dependency wait
+void build_cta_blobs(Schedule& S, const std::vector<int32_t>& pending_rows);
 
 }  // namespace ta

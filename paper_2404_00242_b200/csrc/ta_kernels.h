@@ -72,6 +72,8 @@ struct AttnArgs {
     int out_bf16;
     long long* trace;         // optional clock64 trace (debug builds of the launch: a separate instantiation)
     int prefetch_tiles;       // first tiles of each CTA prefetched into L2 before the dependency wait
+    int early_kv;             // tcgen05 kernel: the CTA's leading tiles that no pending ta_kv_append row
+                              // touches (blob header) are loaded before the dependency wait
     unsigned long long* timeline;   // debug: [4] = attn first start, attn last end, merge first start, merge last end (ns)
 };
 

@@ -1,4 +1,6 @@
-"""CTA spans of the PRODUCT kernel (built with -DTA_LIGHT_TRACE=1, see
+"""CTA spans of the PRODUCT kernel (each mark is a %globaltimer read, which
+itself takes a fraction of a microsecond: consecutive marks with nothing
+between them read ~0.5 us apart, so use differences between distant marks) (built with -DTA_LIGHT_TRACE=1, see
 scripts/build_variant.sh): entry, items done, exit per CTA (globaltimer), over
 isolated launches.   python scripts/light_spans.py [config] [option=value ...]"""
 import os
@@ -93,7 +95,7 @@ for rep in range(8):
         t = tr.cpu().numpy().reshape(n_cta, 256)
         if rep:
             t0 = t[:, 0].min()
-            R.append(np.stack([(t[:, i] - t0) / 1e3 if i != 9 else t[:, 9] for i in (0, 6, 1, 2, 3, 7, 4, 5)], axis=1))
+            R.append(np.stack([(t[:, i] - t0) / 1e3 if i != 9 else t[:, 9] for i in (0, 6, 1, 2, 3, 7, 4, 5, 38, 39, 40)], axis=1))
             ev.append(e0.elapsed_time(e1) * 1e3)
 R = np.stack(R)
 pc = lambda a: " ".join(f"{x:6.2f}" for x in np.percentile(a, [0, 10, 50, 90, 100]))
@@ -108,7 +110,7 @@ print("  last exit    ", pc(R[:, :, 2].max(axis=1)))
 print("  exit - last items done", pc(R[:, :, 2] - R[:, :, 1].max(axis=1, keepdims=True)))
 nt = np.array([S["cta_tiles"][c] for c in range(n_cta)]) if "cta_tiles" in S else None
 ok = ~np.isnan(R[:, :, 3]) & (R[:, :, 3] > -1e5)
-for nm, i in (("first K issue", 3), ("first P", 4), ("P tile 4", 5), ("last P", 6), ("last copy issued", 7)):
+for nm, i in (("TMEM + barriers", 8), ("head landed", 9), ("after pdl wait", 10), ("first K issue", 3), ("first P", 4), ("P tile 4", 5), ("last P", 6), ("last copy issued", 7)):
     v = R[:, :, i]
     v = v[(v > -1e5) & (v < 1e5)]
     print(f"  {nm:16s}", pc(v))
