@@ -139,7 +139,7 @@ static_assert(NBAR * 8 <= TMEM_SLOT, "barriers overlap the TMEM slot");
 // seen by softmax, [+2] S loaded + masked, [+3] row max exchanged, [+4]
 // O_FULL(t-1) seen, [+5] O rescaled, [+6] P published, [+7] item epilogue
 // done (last tile of an item only).
-constexpr int TRACE_SLOTS = 256, TRACE_TILES = 27;   // tiles: slots 8..223
+constexpr int TRACE_SLOTS = 256, TRACE_TILES = 20;   // tiles: slots 8..167 (168.. phase marks)
 __device__ __forceinline__ long long gtimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");

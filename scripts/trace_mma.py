@@ -13,7 +13,7 @@ import torch
 
 import bench
 
-NT = 27   # traced tiles per CTA (TRACE_TILES in csrc/attn_mma.cu)
+NT = 20   # traced tiles per CTA (TRACE_TILES in csrc/attn_mma.cu)
 from paper_2404_00242_b200 import TreeAttention
 
 name = sys.argv[1] if len(sys.argv) > 1 and "=" not in sys.argv[1] else "few_shot"
