@@ -631,6 +631,21 @@ def measure_prefix_split(name, cfg, args, world, rank, local_rank):
                     "NCCL all_to_all_single by head slice, ta_lse_merge -> this rank's heads (bf16)"}
 
 
+# ------------------------------------------------ external B200 baseline
+def external_baseline(timeout=600):
+    """flashinfer's two-level cascade and plain paged decode on config B's tree
+    (scripts/flashinfer_baseline.py), same GPU, same shapes:
+    library kernels as a comparison point, run in a subprocess so a JIT or
+    import failure cannot take the bench line with it."""
+    import subprocess
+    try:
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "flashinfer_baseline.py")],
+                           capture_output=True, text=True, timeout=timeout)
+        return json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else {"error": r.stderr[-300:]}
+    except Exception as e:   # noqa: BLE001 -- a baseline must never sink the line
+        return {"error": str(e)[:300]}
+
+
 # ---------------------------------------------------------- trace replay
 # Paper Table 10 (end-to-end KV IO, TB, DeFT-Flatten; Llama-3-8B counted as 32
 # heads, io_model.hpp:144-146) and Table 8 (attention latency, s, A100 80GB),
@@ -815,6 +830,9 @@ def main():
             split = measure_prefix_split(args.config, cfg, args, world, rank, local_rank)
         except Exception as e:
             split = {"error": str(e)[:300]}
+    external = None
+    if world == 1 and not args.headline_only and args.config == "few_shot":
+        external = external_baseline()
     replays = {}
     if world == 1 and not args.headline_only and not args.no_replay and args.config == "few_shot":
         for name in REPLAY_PRESETS:
@@ -860,6 +878,8 @@ def main():
         line["trace_replay"] = replays
     if split:
         line["prefix_split"] = split
+    if external:
+        line["external_baseline"] = external
     print(json.dumps(line))
     if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
