@@ -595,7 +595,7 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     const int max_rows = opt.use_mma ? opt.max_rows : opt.fma_max_rows;
     const int S_max = std::max(1, max_rows / std::max(1, G));
     const int TG = std::clamp(opt.tile_groups, 1, 8);
-    if (S_max > 4095) fail(TA_ERR_INVALID_ARGUMENT, "schedule: too many slots per lane");
+    if (S_max > 128) fail(TA_ERR_INVALID_ARGUMENT, "schedule: more than 128 slots per lane");
 
     // ---- 1. stripes
     S.kv_tokens_unique = t.total_tokens();   // one pass over the tree's KV (ablation plans load more)
@@ -824,21 +824,39 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
         }
         auto cost = [&](int64_t a, int64_t b) { return P[b] - P[a] + (int64_t)item_cost * (1 + NB[b - 1] - NB[a]); };
         auto runs = [&](int64_t cap, std::vector<int64_t>* cuts) {
-            int64_t a = 0;
+            int64_t a = 0, guess = std::max<int64_t>(1, N / n_cta);
             int n = 0;
             while (a < N) {
-                // the largest b with cost(a, b) <= cap (at least a + 1): gallop, then bisect
-                int64_t step = 1, ok = a + 1;
-                while (ok + step <= N && cost(a, ok + step) <= cap) {
-                    ok += step;
-                    step *= 2;
+                // the largest b with cost(a, b) <= cap (at least a + 1): gallop from
+                // the previous run's length (runs are similar), then bisect
+                int64_t lo, hi;
+                const int64_t g = std::min(N, a + guess);
+                if (g == a + 1 || cost(a, g) <= cap) {
+                    int64_t step = std::max<int64_t>(1, guess / 4);
+                    lo = g;
+                    while (lo + step <= N && cost(a, lo + step) <= cap) {
+                        lo += step;
+                        step *= 2;
+                    }
+                    hi = std::min(N, lo + step - 1);
+                } else {
+                    // cost(a, g) > cap: the answer is in [a + 1, top]; gallop down
+                    int64_t step = std::max<int64_t>(1, guess / 4), top = g - 1, bot = top - step;
+                    while (bot > a && cost(a, bot) > cap) {
+                        top = bot - 1;
+                        step *= 2;
+                        bot = top - step;
+                    }
+                    lo = std::max(a + 1, bot);
+                    hi = std::max(lo, top);
+                    if (cost(a, lo) > cap) hi = lo;   // a single position over the cap still forms a run
                 }
-                int64_t lo = ok, hi = std::min(N, ok + step - 1);
                 while (lo < hi) {
                     const int64_t mid = (lo + hi + 1) / 2;
                     if (cost(a, mid) <= cap) lo = mid; else hi = mid - 1;
                 }
                 if (cuts) cuts->push_back(lo);
+                guess = std::max<int64_t>(1, lo - a);
                 a = lo;
                 if (++n > n_cta && !cuts) return n;   // infeasible budget: stop counting
             }
@@ -902,21 +920,35 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
     // ---- 4. outputs: touched slots, direct vs partial, merge lists
     const int L = S.n_leaves;
     std::vector<int32_t> cover((size_t)L * n_heads, 0);
-    std::vector<int32_t> touched;   // slot-range coverage as a difference array: O(groups + slots)
-    for (ItemDesc& it : S.items) {
-        touched.assign(it.n_slots + 1, 0);
-        for (int i = it.tile_begin; i < it.tile_end; ++i) {
-            const TileDesc& td = S.tiles[i];
-            for (int g = 0; g < td.ng; ++g) {
-                const uint32_t info = S.grp_info[td.grp_begin + g];
-                touched[(info >> 8) & 0xfffu]++;
-                touched[info >> 20]--;
-            }
+    // slots a tile attends, as a 128-bit mask (a lane has <= 128 slots): built
+    // once per tile, OR-ed over an item's tiles (items of every head share them)
+    static thread_local std::vector<uint64_t> tmask;
+    tmask.assign(2 * S.tiles.size(), 0);
+    auto range_bits = [](int lo, int hi, uint64_t& w0, uint64_t& w1) {   // bits [lo, hi)
+        auto word = [](int lo_, int hi_) -> uint64_t {   // within one 64-bit word, 0 <= lo_ <= hi_ <= 64
+            if (hi_ <= lo_) return 0;
+            const uint64_t top = hi_ == 64 ? ~0ull : ((1ull << hi_) - 1);
+            return top & ~((1ull << lo_) - 1);
+        };
+        w0 |= word(std::min(lo, 64), std::min(hi, 64));
+        w1 |= word(std::max(lo, 64) - 64, std::max(hi, 64) - 64);
+    };
+    for (std::size_t i = 0; i < S.tiles.size(); ++i) {
+        const TileDesc& td = S.tiles[i];
+        for (int g = 0; g < td.ng; ++g) {
+            const uint32_t info = S.grp_info[td.grp_begin + g];
+            range_bits((int)((info >> 8) & 0xfffu), (int)(info >> 20), tmask[2 * i], tmask[2 * i + 1]);
         }
-        for (int j = 1; j <= it.n_slots; ++j) touched[j] += touched[j - 1];
+    }
+    for (ItemDesc& it : S.items) {
+        uint64_t m0 = 0, m1 = 0;
+        for (int i = it.tile_begin; i < it.tile_end; ++i) {
+            m0 |= tmask[2 * i];
+            m1 |= tmask[2 * i + 1];
+        }
         it.out_begin = (int32_t)S.slot_out.size();
         for (int j = 0; j < it.n_slots; ++j) {
-            if (touched[j]) {
+            if ((j < 64 ? m0 >> j : m1 >> (j - 64)) & 1ull) {
                 cover[(size_t)S.slot_leaf[it.slot_begin + j] * n_heads + it.head]++;
                 S.slot_out.push_back(0);
             } else {
