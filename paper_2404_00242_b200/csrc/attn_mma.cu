@@ -4,9 +4,9 @@
 // tiles of one lane for one kv head, see ta_internal.h).  Rows of an item
 // are (query slot, q head in the GQA group) pairs, <= 128 of them, one per
 // TMEM lane.  Per tile (<= 8 groups of 16 pool rows = <= 128 tokens):
-//   TMA (warp 0)    K/V boxes -> SMEM ring (128B swizzle), 2 stages, K and V
-//                   on separate barriers; runs ahead across items.  Two stages
-//                   per SM already keep HBM saturated; a deeper ring only adds
+//   TMA (warp 0)    K/V boxes -> separate K and V rings (128B swizzle), 2
+//                   stages each; runs ahead across items.  Two stages per SM
+//                   already keep HBM saturated; a deeper ring only adds
 //                   queueing latency (paid at every CTA's start and end)
 //   QK  (warp 1)    S = Q K^T  (M=128, N=16*groups, K=128), Q from TMEM
 //                   -> S buffer (t & 1) in TMEM
@@ -22,12 +22,14 @@
 // At an item's end the softmax warps write each attended row either as the
 // final output (its leaf-head is covered by this item alone) or as an
 // (O/l, log2 lse) partial record, by bulk async copies.
+// Schedule staging: the CTA's per-CTA blob (ta_internal.h, namespace blob),
+// a fixed head by one bulk copy, the tail behind it.
 // Fused merge (no merge launch): at its end, once its copies have landed, a
 // CTA publishes how many partials it wrote per merge record, then merges the
-// records it owns (it wrote their last partial): it waits only for lower
-// CTAs, which publish before they merge themselves, so with every CTA
-// resident (<= one per SM) there is no wait cycle.  Otherwise merge.cu runs
-// as a second launch.
+// records it owns (owners spread evenly by merge work; two rows per warp).
+// Every CTA publishes before it waits and every CTA is resident (<= one per
+// SM), so no wait can block a publication.  The FMA kernel's schedules use
+// merge.cu as a second launch instead.
 //
 // Reference semantics: group_attention (attention.hpp:117-204) over every
 // chunk a leaf attends; tree_reduce (attention.hpp:209-233) at the owner

@@ -568,8 +568,8 @@ std::string plan_json(const Tree& t, const Plan& p) {
 //    run's maximal (head, lane) pieces are its items.
 // 4. Outputs.  A leaf-head attended by one item is written directly; else
 //    its items write partials that are merged in item order (tree_reduce,
-//    attention.hpp:209-233): at the end of the attention launch by the highest
-//    CTA that wrote one of them (fused merge) or by the merge launch after it.
+//    attention.hpp:209-233): at the end of the attention launch by the record's
+//    owner CTA (fused merge) or by the merge launch after it.
 // ===========================================================================
 namespace {
 

@@ -141,8 +141,8 @@ std::string plan_json(const Tree& t, const Plan& p);           // serde.hpp:41-6
 // Items whose leaf-head is covered by one item write the final output
 // directly.  Otherwise the leaf-head's items write (O/l, log2 lse) partial
 // records, merged in item order (deterministic): at the end of the attention
-// launch by the highest CTA that wrote one of them (fused merge), or by the
-// merge launch.
+// launch by the record's owner CTA (fused merge, tcgen05 kernel), or by the
+// merge launch (FMA kernel).
 struct TileDesc {          // 16 bytes, read by the device
     int32_t grp_begin;     // into grp_row / grp_info
     uint8_t ng;            // groups in the tile (1..8)
@@ -268,8 +268,8 @@ struct SchedOptions {
     int fma_max_rows = 8;      // rows per lane of the FMA kernel (8 or 16)
     bool final_direct = true;  // single-item leaf-heads written directly
     bool fused_merge = false;  // split leaf-heads merged inside the attention launch, at the end of the
-                               // highest CTA that wrote one of their partials (tcgen05 kernel, all CTAs
-                               // co-resident); else by the merge launch
+                               // record's owner CTA after every CTA has published its partial counts
+                               // (tcgen05 kernel, all CTAs co-resident); else by the merge launch
     int64_t trace_ptr = 0;     // debug: device buffer for the kernel's clock64 trace
 };
 
