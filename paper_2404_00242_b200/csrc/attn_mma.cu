@@ -121,6 +121,9 @@ constexpr float kLazy = 8.0f;                            // rescale O only when 
             }                                                                                      \
         }                                                                                          \
     } while (0)
+#ifndef TA_ABL_NOMERGE
+#define TA_ABL_NOMERGE 0  // publish but do not wait / merge (timing only)
+#endif
 #ifndef TA_ABL_NOPUB
 #define TA_ABL_NOPUB 0    // no fused merge (timing only)
 #endif
@@ -804,7 +807,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int G = a.G;
         // two rows per warp (half-warp merges): every owned row in one round
         const int hw = lane >> 4;
-        for (int row0 = 2 * warp; row0 < n_own * G; row0 += 2 * (NTHREADS / 32)) {
+        for (int row0 = TA_ABL_NOMERGE ? n_own * G : 2 * warp; row0 < n_own * G; row0 += 2 * (NTHREADS / 32)) {
             const int row = row0 + hw;
             const bool active = row < n_own * G;
             const int k = active ? row / G : 0;
