@@ -332,8 +332,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (k < HI) {   // else its item is in the tail
             const int64_t row0 = a.layer_row0 + (int64_t)s_item[k].head * a.head_rows;
             const TileDesc td = s_td[lane];
-            for (int b = 0; b < td.nbox; ++b) {
-                const int g = td.box[b] >> 2, sz = td.box[b] & 3;
+            uint64_t boxes;
+            std::memcpy(&boxes, td.box, 8);
+#pragma unroll 1
+            for (int b = 0; b < td.nbox; ++b, boxes >>= 8) {
+                const int g = (int)(boxes & 0xffu) >> 2, sz = (int)(boxes & 3u);
                 const int row = (int)(row0 + s_tm[lane].row[g]);
                 tma_prefetch_2d(&tm.k[sz], 0, row);
                 tma_prefetch_2d(&tm.k[sz], 64, row);
@@ -415,8 +418,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const uint32_t bytes = (uint32_t)td.ng * 4096u;
                     mbar_wait(BAR(EMPTYK + s), ph ^ 1);
                     mbar_expect_tx(BAR(FULLK + s), bytes);
-                    for (int b = 0; b < td.nbox; ++b) {
-                        const int g = td.box[b] >> 2, sz = td.box[b] & 3;
+                    uint64_t boxes;   // the 8 box codes in a register (no local-memory indexing)
+                    std::memcpy(&boxes, td.box, 8);
+#pragma unroll 1   // rolled: unrolled TMA issue sequences bloated the kernel's code (I-cache)
+                    for (int b = 0; b < td.nbox; ++b, boxes >>= 8) {
+                        const int g = (int)(boxes & 0xffu) >> 2, sz = (int)(boxes & 3u);
                         const int row = (int)(row0 + tmp->row[g]);
                         tma_load_2d(kdst + g * 2048, &tm.k[sz], 0, row, BAR(FULLK + s));
                         tma_load_2d(kdst + HALF + g * 2048, &tm.k[sz], 64, row, BAR(FULLK + s));
@@ -426,8 +432,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (gt == 0) TA_LIGHT(2, bytes);
                     mbar_wait(BAR(EMPTYV + sv), phv ^ 1);
                     mbar_expect_tx(BAR(FULLV + sv), bytes);
-                    for (int b = 0; b < td.nbox; ++b) {
-                        const int g = td.box[b] >> 2, sz = td.box[b] & 3;
+                    std::memcpy(&boxes, td.box, 8);
+#pragma unroll 1
+                    for (int b = 0; b < td.nbox; ++b, boxes >>= 8) {
+                        const int g = (int)(boxes & 0xffu) >> 2, sz = (int)(boxes & 3u);
                         const int row = (int)(row0 + tmp->row[g]);
                         tma_load_2d(vdst + g * 2048, &tm.v[sz], 0, row, BAR(FULLV + sv));
                         tma_load_2d(vdst + HALF + g * 2048, &tm.v[sz], 64, row, BAR(FULLV + sv));
