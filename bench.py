@@ -533,11 +533,16 @@ def measure_decode_loop(name, cfg, args, world, rank, local_rank):
 
     host = []
 
+    prep = []
+
     def step():
         h0 = time.perf_counter()
         ctx.append_leaves()
+        h1 = time.perf_counter()
         ctx.prepare(128, stream)
-        host.append(time.perf_counter() - h0)
+        h2 = time.perf_counter()
+        host.append(h2 - h0)
+        prep.append(h2 - h1)
         if state["graph"] is None or ctx.graph_epoch() != state["epoch"]:
             torch.cuda.synchronize()
             state["epoch"] = ctx.graph_epoch()
@@ -551,6 +556,8 @@ def measure_decode_loop(name, cfg, args, world, rank, local_rank):
         step()
     torch.cuda.synchronize()
     host.clear()
+    prep.clear()
+    fast0 = ctx.fast_prepares()
     rec0 = state["recaptures"]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -569,6 +576,8 @@ def measure_decode_loop(name, cfg, args, world, rank, local_rank):
                                "total": (io.host_plan_ns + io.host_schedule_ns + io.host_upload_ns) / 1e3},
            "iterations": [it0 + W + 1, it0 + W + K], "graph_recaptures_in_timed_steps": state["recaptures"] - rec0,
            "kv_append_rows_per_step": ctx.kv_append_rows(), "gpu_launches_per_step": L_layers * (1 + ctx.launches_per_attend()),
+           "fast_prepares_in_timed_steps": ctx.fast_prepares() - fast0,
+           "host_prepare_us_per_step_incl_backpressure": {"median": statistics.median(prep) * 1e6, "max": max(prep) * 1e6},
            "kv_bytes_per_layer_at_end": io.kv_bytes,
            "path": "per step: ta_tree_append_leaves (1 token per leaf) + ta_prepare, then one graph replay of "
                    "n_layers x (ta_kv_append + ta_attend)"}

@@ -196,6 +196,12 @@ ta_status ta_io_analytical(ta_ctx* ctx, int algorithm, const ta_cost_params* par
  * that wait (off by default; a caller that writes the pools by other means
  * on the same stream must leave it off). */
 ta_status ta_prepare(ta_ctx* ctx, int block_size, void* stream);
+/* Decode-step fast path of ta_prepare: when the only mutations since the last
+ * ta_prepare are ta_tree_append_leaves and every new token extends its leaf's
+ * tail group of the current device schedule (same page, group not full), the
+ * schedule is patched in place instead of re-planned (the flatten plan is
+ * rebuilt on demand by the plan queries).  Number of such prepares so far. */
+int64_t ta_fast_prepares(ta_ctx* ctx);
 ta_status ta_attend(ta_ctx* ctx, int layer, const void* q, void* out, float* lse, void* stream);
 /* End-to-end variant over HOST buffers (pinned or pageable): H2D q, attend,
  * D2H out, synchronised on `stream` before returning. */

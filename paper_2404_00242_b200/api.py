@@ -334,6 +334,10 @@ class TreeAttention:
     def attend_host_wait(self):
         check(lib().ta_attend_host_wait(self._h), "attend_host_wait")
 
+    def fast_prepares(self) -> int:
+        """prepare() calls that patched the schedule in place (decode-step fast path)."""
+        return int(lib().ta_fast_prepares(self._h))
+
     def io_stats(self) -> IoStats:
         s = capi.IoStats()
         check(lib().ta_io_stats_get(self._h, C.byref(s)), "io_stats")

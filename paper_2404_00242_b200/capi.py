@@ -29,7 +29,7 @@ EXPORTED = [
     "ta_kv_write", "ta_plan_flatten", "ta_plan_json", "ta_prepare", "ta_attend", "ta_attend_host", "ta_attend_host_async", "ta_attend_host_wait",
     "ta_io_stats_get", "ta_launches_per_attend", "ta_schedule_get",
     "ta_tree_append_leaves", "ta_kv_append", "ta_kv_append_rows", "ta_graph_epoch",
-    "ta_io_measured", "ta_io_analytical", "ta_lse_merge",
+    "ta_io_measured", "ta_io_analytical", "ta_lse_merge", "ta_fast_prepares",
 ]
 
 TA_STRATEGY = {"q-guided": 0, "node": 1, "node-chunk": 2, "flatten": 3}
@@ -166,6 +166,7 @@ def lib():
         "ta_kv_append": (C.c_int, [vp, C.c_int, vp, vp, vp]),
         "ta_kv_append_rows": (i64, [vp]),
         "ta_graph_epoch": (i64, [vp]),
+        "ta_fast_prepares": (i64, [vp]),
         "ta_io_measured": (C.c_int, [vp, C.c_int, C.POINTER(CostParams), C.POINTER(IoReport)]),
         "ta_io_analytical": (C.c_int, [vp, C.c_int, C.POINTER(CostParams), C.c_int, C.POINTER(IoReport)]),
         "ta_lse_merge": (C.c_int, [vp, vp, C.c_int, i64, C.c_int, vp, C.c_int, vp, vp]),

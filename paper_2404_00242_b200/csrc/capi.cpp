@@ -35,6 +35,12 @@ struct ta_ctx {
     bool prepared = false;
     uint64_t prepared_version = ~0ull;
     int prepared_bs = -1;
+    // decode-step fast path: tokens appended by ta_tree_append_leaves since the
+    // last ta_prepare, as (leaf, token index), while no other mutation happened
+    std::vector<std::pair<int32_t, int64_t>> fast_log;
+    uint64_t fast_log_version = ~0ull;   // tree version after the last logged append
+    bool fast_bad = true;
+    int64_t n_fast_prepares = 0;
 
     // TMA descriptors (CUtensorMap, 128 B) over the whole K / V pools
     alignas(64) unsigned char tmap_k[512];   // CUtensorMap for 16/32/64/128-row boxes
@@ -432,15 +438,24 @@ ta_status ta_tree_append_leaves(ta_ctx* c, int n, const int32_t* leaves, const i
         if (c->pool.capacity >= 0 &&
             pages > (int64_t)c->pool.free_list.size() + c->pool.capacity - (int64_t)c->pool.pages.size())
             fail(TA_ERR_OUT_OF_MEMORY, "append_leaves: device page capacity exhausted");
+        const uint64_t v0 = c->tree.version;
+        const bool chain = c->prepared && !c->fast_bad &&
+                           (c->fast_log.empty() ? v0 == c->prepared_version : v0 == c->fast_log_version);
         for (size_t i = 0; i < ids.size(); ++i) {
             const int64_t k = counts ? counts[i] : 1, t0 = c->tree.count[ids[i]];
             c->tree.append(ids[i], k);
             queue_rows(c, ids[i], t0, k);
+            if (chain)
+                for (int64_t j = 0; j < k; ++j) c->fast_log.push_back({ids[i], t0 + j});
         }
+        if (chain) c->fast_log_version = c->tree.version;
+        else c->fast_bad = true;
     });
 }
 
 int64_t ta_graph_epoch(ta_ctx* c) { return c ? c->graph_epoch : -1; }
+
+int64_t ta_fast_prepares(ta_ctx* c) { return c ? c->n_fast_prepares : -1; }
 
 ta_status ta_kv_append(ta_ctx* c, int layer, const void* k, const void* v, void* stream) {
     return guard([&] {
@@ -843,6 +858,25 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
         // one decode step = plan + schedule + metadata upload, reused by every layer
         const auto t0 = std::chrono::steady_clock::now();
+        // decode-step fast path: only ta_tree_append_leaves since the last
+        // prepare, and every new token extends its leaf's tail group -> patch the
+        // schedule in place (the flatten plan is rebuilt on demand only).  Off
+        // with early_kv (its per-CTA early-tile counts depend on the new rows).
+        if (c->prepared && !c->fast_bad && !c->fast_log.empty() && c->tree.version == c->fast_log_version &&
+            c->prepared_bs == bs && c->strategy == TA_STRATEGY_FLATTEN && c->sched.fused_merge && !c->early_kv &&
+            patch_schedule_appends(c->sched, c->pool, c->fast_log)) {
+            const auto t2f = std::chrono::steady_clock::now();
+            c->plan_valid = false;
+            upload_schedule(c, (cudaStream_t)stream);
+            c->t_plan_ns = 0;
+            c->t_sched_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t2f - t0).count();
+            c->prepared_version = c->tree.version;
+            c->fast_log.clear();
+            ++c->n_fast_prepares;
+            return;
+        }
+        c->fast_log.clear();
+        c->fast_bad = false;
         make_plan(c->tree, c->strategy, bs, c->plan);
         const auto t1 = std::chrono::steady_clock::now();
         c->plan_valid = true;
@@ -861,6 +895,7 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             c->pending_sorted.assign(c->pending_rows.begin(), c->pending_rows.end());
             std::sort(c->pending_sorted.begin(), c->pending_sorted.end());
             build_cta_blobs(c->sched, c->pending_sorted);
+            if (c->sched.fused_merge) build_tail_map(c->tree, c->pool, c->sched);
         }
         const auto t2 = std::chrono::steady_clock::now();
         upload_schedule(c, (cudaStream_t)stream);

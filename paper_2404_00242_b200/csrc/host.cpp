@@ -6,6 +6,8 @@
 #include <atomic>
 #include <cstdio>
 #include <numeric>
+#include <unordered_map>
+#include <cstddef>
 
 #include "ta_internal.h"
 #include "treeattn_b200.h"
@@ -1084,6 +1086,8 @@ void build_cta_blobs(Schedule& S, const std::vector<int32_t>& pending_rows) {
     std::vector<int32_t> slots;
     std::vector<TileDesc> tds;
     std::vector<TileMeta> tms;
+    std::vector<int32_t> tids;   // global tile index of each staged tile
+    std::vector<std::pair<int32_t, uint32_t>> copies;   // (tile, blob offset of its TileMeta copy)
     for (int c = 0; c < n_cta; ++c) {
         uint8_t* head = S.cta_heads.data() + (size_t)c * HEAD_BYTES;
         int32_t* hdr = reinterpret_cast<int32_t*>(head + HDR);
@@ -1093,6 +1097,7 @@ void build_cta_blobs(Schedule& S, const std::vector<int32_t>& pending_rows) {
         const int ni_s = std::min(ni, MAXI);
         tds.clear();
         tms.clear();
+        tids.clear();
         slots.clear();
         int off = 0, so = 0;
         for (int k = 0; k < ni_s; ++k) {
@@ -1104,6 +1109,7 @@ void build_cta_blobs(Schedule& S, const std::vector<int32_t>& pending_rows) {
             for (int t = it.tile_begin; t < it.tile_end && (int)tds.size() < MAXT; ++t) {
                 tds.push_back(S.tiles[t]);
                 tms.push_back(S.tile_meta[t]);
+                tids.push_back(t);
             }
             for (int j = 0; j < it.n_slots && (int)slots.size() < MAXS; ++j) slots.push_back(S.slot_leaf[it.slot_begin + j]);
         }
@@ -1151,6 +1157,9 @@ void build_cta_blobs(Schedule& S, const std::vector<int32_t>& pending_rows) {
         if (nt_s > HT) put(S.cta_tails, tds.data() + HT, (size_t)(nt_s - HT) * sizeof(TileDesc));
         hdr[T_TD] = (int32_t)(S.cta_tails.size() - b0);
         b0 = S.cta_tails.size();
+        for (int lt = 0; lt < nt_s; ++lt)
+            copies.push_back({tids[lt], lt < HT ? (uint32_t)((size_t)c * HEAD_BYTES + H_TM + lt * sizeof(TileMeta))
+                                                 : (uint32_t)(b0 + (lt - HT) * sizeof(TileMeta)) | 0x80000000u});
         if (nt_s > HT) put(S.cta_tails, tms.data() + HT, (size_t)(nt_s - HT) * sizeof(TileMeta));
         hdr[T_TM] = (int32_t)(S.cta_tails.size() - b0);
         b0 = S.cta_tails.size();
@@ -1171,6 +1180,71 @@ void build_cta_blobs(Schedule& S, const std::vector<int32_t>& pending_rows) {
         hdr[T_PUB] = (int32_t)(S.cta_tails.size() - b0);
     }
     if (S.cta_tails.empty()) S.cta_tails.resize(16, 0);
+    // copies by tile (counting sort)
+    S.tile_copy_begin.assign(S.tiles.size() + 1, 0);
+    for (const auto& cp : copies) S.tile_copy_begin[cp.first + 1]++;
+    for (size_t t = 0; t < S.tiles.size(); ++t) S.tile_copy_begin[t + 1] += S.tile_copy_begin[t];
+    S.tile_copy.assign(copies.size(), 0);
+    std::vector<int32_t> pos(S.tile_copy_begin.begin(), S.tile_copy_begin.end() - 1);
+    for (const auto& cp : copies) S.tile_copy[pos[cp.first]++] = cp.second;
+}
+
+void build_tail_map(const Tree& t, const PagePool& pool, Schedule& S) {
+    S.grp_tile.assign(S.grp_row.size(), -1);
+    for (size_t i = 0; i < S.tiles.size(); ++i)
+        for (int g = 0; g < S.tiles[i].ng; ++g) S.grp_tile[S.tiles[i].grp_begin + g] = (int32_t)i;
+    // a leaf's last token is the last row of its group (nothing follows it in its page)
+    std::unordered_map<int32_t, int32_t> last_row;   // pool row -> group
+    last_row.reserve(S.grp_row.size() * 2);
+    for (size_t g = 0; g < S.grp_row.size(); ++g) last_row[S.grp_row[g] + (int32_t)(S.grp_info[g] & 0xffu) - 1] = (int32_t)g;
+    S.tail_grp.assign(t.alive.size(), -1);
+    const int P = pool.page_size;
+    for (int32_t leaf : t.leaves) {
+        const int64_t n = t.count[leaf];
+        if (n == 0) continue;
+        const auto& h = pool.handle(leaf);
+        const int32_t row = (int32_t)(h.pages[(n - 1) / P] * P + (n - 1) % P);
+        auto it = last_row.find(row);
+        if (it != last_row.end()) S.tail_grp[leaf] = it->second;
+    }
+}
+
+bool patch_schedule_appends(Schedule& S, const PagePool& pool,
+                            const std::vector<std::pair<int32_t, int64_t>>& appends) {
+    if (S.tail_grp.empty() || S.tile_copy_begin.empty()) return false;
+    const int P = pool.page_size;
+    // dry run: every token extends its leaf's tail group by the next pool row
+    std::unordered_map<int32_t, int32_t> cnt;   // group -> count after the appends so far
+    for (const auto& [leaf, tok] : appends) {
+        if (leaf < 0 || leaf >= (int32_t)S.tail_grp.size() || S.tail_grp[leaf] < 0) return false;
+        const int32_t g = S.tail_grp[leaf];
+        auto it = cnt.find(g);
+        const int32_t c0 = it != cnt.end() ? it->second : (int32_t)(S.grp_info[g] & 0xffu);
+        const auto& h = pool.handle(leaf);
+        const int32_t row = (int32_t)(h.pages[tok / P] * P + tok % P);
+        if (c0 >= 16 || S.grp_row[g] + c0 != row) return false;
+        cnt[g] = c0 + 1;
+    }
+    // apply: the group's count in grp_info, in the tile metadata and in every
+    // CTA blob's copy of it
+    for (const auto& [g, c] : cnt) {
+        const uint32_t info = S.grp_info[g];
+        const uint32_t ninfo = (info & ~0xffu) | (uint32_t)c;
+        const int added = c - (int)(info & 0xffu);
+        S.grp_info[g] = ninfo;
+        const int32_t t = S.grp_tile[g];
+        const int gi = g - S.tiles[t].grp_begin;
+        S.tile_meta[t].info[gi] = ninfo;
+        S.tiles[t].ntok = (uint16_t)(S.tiles[t].ntok + added);
+        for (int32_t k = S.tile_copy_begin[t]; k < S.tile_copy_begin[t + 1]; ++k) {
+            const uint32_t off = S.tile_copy[k];
+            uint8_t* base = (off & 0x80000000u) ? S.cta_tails.data() + (off & 0x7fffffffu) : S.cta_heads.data() + off;
+            std::memcpy(base + offsetof(TileMeta, info) + 4 * gi, &ninfo, 4);
+        }
+    }
+    S.kv_tokens_unique += (int64_t)appends.size();
+    S.masked_q_tokens += (int64_t)appends.size();   // each new token is on exactly one leaf's path
+    return true;
 }
 
 }  // namespace ta

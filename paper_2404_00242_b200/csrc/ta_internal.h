@@ -226,6 +226,14 @@ struct Schedule {
     std::vector<Pub> cta_pub;
     std::vector<int32_t> cta_own_begin;   // [n_ctas + 1] into cta_own
     std::vector<int32_t> cta_own;         // merge records
+    // decode-step fast path (tcgen05 schedules, patch_schedule_appends): per
+    // node id the group holding a leaf's last token (-1: none), group -> tile,
+    // and where the CTA blobs keep copies of each tile's TileMeta (byte offsets;
+    // bit 31 set: into cta_tails, else into cta_heads)
+    std::vector<int32_t> tail_grp;
+    std::vector<int32_t> grp_tile;
+    std::vector<int32_t> tile_copy_begin;
+    std::vector<uint32_t> tile_copy;
     std::vector<uint8_t> cta_heads;   // [n_ctas][blob::HEAD_BYTES]
     std::vector<uint8_t> cta_tails;   // packed tails (16-byte sections)
     std::vector<int32_t> empty;       // [n][2] (leaf, local head) pairs with no path tokens
@@ -245,6 +253,7 @@ struct Schedule {
         fused_merge = false;
         cta_pub_begin.clear(); cta_pub.clear(); cta_own_begin.clear(); cta_own.clear();
         cta_heads.clear(); cta_tails.clear();
+        tail_grp.clear(); grp_tile.clear(); tile_copy_begin.clear(); tile_copy.clear();
         n_lanes = n_partials = n_leaves = max_lane_rows = 0;
         kv_tokens_unique = kv_rows_loaded = masked_q_tokens = n_stripes = 0;
     }
@@ -275,6 +284,14 @@ struct SchedOptions {
 
 void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int group_size,
                     int n_kv_heads_local, const SchedOptions& opt, Schedule& out);
+// Decode-step fast path: the leaf-tail map of a built schedule (after
+// build_cta_blobs), and the in-place patch for tokens appended to leaves since
+// (leaf node, token index) -- every new token must extend its leaf's tail group
+// by the next pool row (same page, group not full); false (nothing changed)
+// otherwise, and the caller rebuilds.
+void build_tail_map(const Tree& t, const PagePool& pool, Schedule& S);
+bool patch_schedule_appends(Schedule& S, const PagePool& pool,
+                            const std::vector<std::pair<int32_t, int64_t>>& appends);
 // per-CTA head / tail blobs of a built schedule (tcgen05 kernel)
 // pending_rows: pool rows the step's ta_kv_append writes (sorted); a CTA's
 // leading tiles without any of them may be loaded before the dependency wait
