@@ -54,6 +54,15 @@ constexpr int DH = 128;                                  // head dim
 #ifndef TA_NV
 #define TA_NV 2
 #endif
+#ifndef TA_NQ
+#define TA_NQ 2   // threads per softmax row, each owning 128 / TA_NQ columns: 2 or 4
+#endif
+constexpr int NQ = TA_NQ;                                // threads per row (column splits)
+constexpr int CPT = 128 / NQ;                            // S / O / Q columns per softmax thread
+constexpr int GPT = 8 / NQ;                              // 16-column S groups per softmax thread
+constexpr int NTHREADS = 96 + 128 * NQ;                  // 3 issuer warps + 4 * NQ softmax warps
+constexpr int NSOFT = 128 * NQ;                          // softmax threads
+static_assert(NQ == 2 || NQ == 4, "column splits");
 constexpr int NK = TA_NK;                                // K ring depth (a K tile is released by its QK)
 constexpr int NV = TA_NV;                                // V ring depth (a V tile waits for the softmax and PV)
 constexpr int HALF = BM * 128;                           // one 64-column half of a [128][128] bf16 tile
@@ -61,8 +70,8 @@ constexpr int TILE = 2 * HALF;                           // 32 KB
 constexpr int SMEM_K = 0;                                // K stage s at s * TILE
 constexpr int SMEM_V = NK * TILE;                        // V stage s at SMEM_V + s * TILE
 constexpr int SMEM_BAR = SMEM_V + NV * TILE;
-constexpr int SMEM_RED = SMEM_BAR + 256;                 // [2 parity][2 half][128] fp32 row max
-constexpr int SMEM_REDL = SMEM_RED + 2 * 2 * BM * 4;     // [2 half][128] fp32 row sum
+constexpr int SMEM_RED = SMEM_BAR + 256;                 // [2 parity][NQ split][128] fp32 row max
+constexpr int SMEM_REDL = SMEM_RED + 2 * NQ * BM * 4;    // [NQ split][128] fp32 row sum
 // the CTA's schedule (ta_internal.h, namespace blob): header + per-item tile /
 // slot offsets, items, tile descriptors and metadata, slot leaves, and the
 // fused merge's owned records and publications, staged by bulk copies
@@ -74,15 +83,15 @@ using blob::MAXP;
 using blob::HI;
 using blob::HT;
 using blob::HS;
-// epilogue staging: one row of O / l (this thread's 64 columns) per thread,
+// epilogue staging: one row of O / l (this thread's CPT columns) per thread,
 // written to global by bulk async copies
 #ifndef TA_EPI_PASSES
 #define TA_EPI_PASSES 1
 #endif
 constexpr int EPI_PASSES = TA_EPI_PASSES;                // fp32 rows staged in 1 or 2 column passes
-constexpr int EPI_ROW = 256 / EPI_PASSES + 16;
-constexpr int SMEM_EPI = SMEM_REDL + 2 * BM * 4;        // [8 warps][32 rows][EPI_ROW]
-constexpr int SMEM_HDR = SMEM_EPI + 8 * 32 * EPI_ROW;    // blob header + IOFF + SOFF (blob::H_ITEMS bytes)
+constexpr int EPI_ROW = CPT * 4 / EPI_PASSES + 16;
+constexpr int SMEM_EPI = SMEM_REDL + NQ * BM * 4;       // [softmax warps][32 rows][EPI_ROW]
+constexpr int SMEM_HDR = SMEM_EPI + NSOFT * EPI_ROW;     // blob header + IOFF + SOFF (blob::H_ITEMS bytes)
 constexpr int SMEM_ITEM = SMEM_HDR + blob::H_ITEMS;      // ItemDesc[MAXI]
 constexpr int SMEM_TD = SMEM_ITEM + MAXI * 32;           // TileDesc[MAXT]
 constexpr int SMEM_TM = SMEM_TD + MAXT * 16;             // TileMeta[MAXT]
@@ -93,10 +102,8 @@ constexpr int SMEM_PUB = SMEM_OWNID + MAXO * 4;          // int2[MAXP]: (record,
 constexpr int SMEM_BYTES = SMEM_PUB + MAXP * 8 + 1024;   // + alignment slack
 static_assert(SMEM_HDR % 16 == 0 && SMEM_ITEM % 16 == 0 && SMEM_SLOT % 16 == 0 && SMEM_OWN % 16 == 0, "bulk copy alignment");
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
-constexpr int NTHREADS = 352;                           // 3 issuer warps + 8 softmax warps
 constexpr int SOFT0 = 3;                                 // first softmax warp
 constexpr int TRACE_TID = SOFT0 * 32;                    // thread that records the softmax trace
-constexpr int NSOFT = 256;
 constexpr int TMEM_COLS = 512;
 constexpr int TMEM_S = 0, TMEM_O = 256, TMEM_Q = 384;   // S0, S1 (P aliased), O, Q0, Q1 (item parity)
 constexpr float kLazy = 8.0f;                            // rescale O only when the max grows by > 2^8
@@ -350,7 +357,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const ItemDesc I0 = s_item[0];
         if (r < I0.n_slots * a.G && r / a.G < ns_s) {
             const __nv_bfloat16* qp = reinterpret_cast<const __nv_bfloat16*>(a.q) +
-                                      ((size_t)s_slot[r / a.G] * a.hq_loc + I0.head * a.G + r % a.G) * DH + 64 * h;
+                                      ((size_t)s_slot[r / a.G] * a.hq_loc + I0.head * a.G + r % a.G) * DH + CPT * h;
             asm volatile("prefetch.global.L2 [%0];" ::"l"(qp));
         }
     }
@@ -504,7 +511,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else {
         // ===================== softmax / epilogue (256 threads) =====================
         const int q4 = warp & 3;                 // TMEM lane quadrant of this warp (warps 3..10)
-        const int h = (warp - SOFT0) >> 2;       // column half (S groups 4h..4h+3, O / Q columns 64h..)
+        const int h = (warp - SOFT0) >> 2;       // column split (S groups GPT*h.., O / Q columns CPT*h..)
         const int r = q4 * 32 + lane;            // row == TMEM lane
         const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
         const int G = a.G;
@@ -513,24 +520,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // Q row of an item (this thread: dims [64h, 64h+64) of row r = 32
         // packed bf16 pairs) -> registers -> (once the previous item's QK is
         // complete) tcgen05.st into the Q columns
+        constexpr int QV = CPT / 8;   // uint4 of this thread's Q dims
         auto q_row = [&](const ItemDesc& I, int leaf) -> const uint4* {
             return reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.q) +
-                                                  ((size_t)leaf * a.hq_loc + I.head * G + r % G) * DH) + 8 * h;
+                                                  ((size_t)leaf * a.hq_loc + I.head * G + r % G) * DH) + QV * h;
         };
-        auto q_fetch = [&](const ItemDesc& I, int leaf, uint4 (&v)[8]) {
+        auto q_fetch = [&](const ItemDesc& I, int leaf, uint4 (&v)[QV]) {
             if (leaf >= 0) {
                 const uint4* src = q_row(I, leaf);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) v[c] = src[c];
+                for (int c = 0; c < QV; ++c) v[c] = src[c];
             } else {
 #pragma unroll
-                for (int c = 0; c < 8; ++c) v[c] = make_uint4(0, 0, 0, 0);
+                for (int c = 0; c < QV; ++c) v[c] = make_uint4(0, 0, 0, 0);
             }
         };
-        auto q_store = [&](const uint4 (&v)[8], int qb) {
+        auto q_store = [&](const uint4 (&v)[QV], int qb) {
             const uint32_t* w = reinterpret_cast<const uint32_t*>(v);
-            TA_TMEM_ST16(tmem + lane_addr + TMEM_Q + 64 * qb + 32 * h, w);
-            TA_TMEM_ST16(tmem + lane_addr + TMEM_Q + 64 * qb + 32 * h + 16, (w + 16));
+#pragma unroll
+            for (int c = 0; c < QV / 4; ++c) TA_TMEM_ST16(tmem + lane_addr + TMEM_Q + 64 * qb + (CPT / 2) * h + 16 * c, (w + 16 * c));
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(BAR(Q_FULL + qb));
@@ -538,7 +546,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
         if (n_items > 0) {
             const ItemDesc I0 = item_at(0);
-            uint4 qv[8];
+            uint4 qv[QV];
             q_fetch(I0, r < I0.n_slots * G ? leaf_at(0, I0, r / G) : -1, qv);
             q_store(qv, 0);
         }
@@ -563,15 +571,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
                 const TileDesc td = td_at(gt, t);
-                const uint4 inf = *reinterpret_cast<const uint4*>(tm_at(gt, t)->info + 4 * h);
+                uint32_t info[GPT];
+                if constexpr (GPT == 4) {
+                    const uint4 inf = *reinterpret_cast<const uint4*>(tm_at(gt, t)->info + 4 * h);
+                    info[0] = inf.x; info[1] = inf.y; info[2] = inf.z; info[3] = inf.w;
+                } else {
+                    const uint2 inf = *reinterpret_cast<const uint2*>(tm_at(gt, t)->info + 2 * h);
+                    info[0] = inf.x; info[1] = inf.y;
+                }
                 const int ng = td.ng;
-                const int g0 = 4 * h;
-                const uint32_t info[4] = {inf.x, inf.y, inf.z, inf.w};
+                const int g0 = GPT * h;
                 // per group: number of leading columns this row attends (0: none)
-                int lim[4];
+                int lim[GPT];
                 bool att = false;
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
+                for (int g = 0; g < GPT; ++g) {
                     const int b = (int)((info[g] >> 8) & 0xfffu), e = (int)(info[g] >> 20);
                     lim[g] = (live_row && g0 + g < ng && j >= b && j < e) ? (int)(info[g] & 0xffu) : 0;
                     att |= lim[g] > 0;
@@ -582,32 +596,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mbar_wait(BAR(S_FULL + sb), (gt >> 1) & 1);
                 if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 1);
                 tc_fence_after();
-                // S of my half into registers (one pass), tree mask, row max
-                uint32_t r0[16], r1[16], r2[16], r3[16];
+                // S of my column split into registers (one pass), tree mask, row max
+                uint32_t rv[GPT][16];
                 float mx = -INFINITY;
                 if (warp_att && !TA_ABL_STREAM) {
                     // groups past ng hold stale columns; lim == 0 masks them
-                    TA_TMEM_LD16(s_addr + g0 * 16, r0);
-                    TA_TMEM_LD16(s_addr + (g0 + 1) * 16, r1);
-                    TA_TMEM_LD16(s_addr + (g0 + 2) * 16, r2);
-                    TA_TMEM_LD16(s_addr + (g0 + 3) * 16, r3);
+#pragma unroll
+                    for (int g = 0; g < GPT; ++g) TA_TMEM_LD16(s_addr + (g0 + g) * 16, rv[g]);
                     tmem_wait_ld();
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
-                        r0[c] = c < lim[0] ? r0[c] : 0xff800000u;   // -inf
-                        r1[c] = c < lim[1] ? r1[c] : 0xff800000u;
-                        r2[c] = c < lim[2] ? r2[c] : 0xff800000u;
-                        r3[c] = c < lim[3] ? r3[c] : 0xff800000u;
-                        mx = fmaxf(fmaxf(mx, fmaxf(__uint_as_float(r0[c]), __uint_as_float(r1[c]))),
-                                   fmaxf(__uint_as_float(r2[c]), __uint_as_float(r3[c])));
+#pragma unroll
+                        for (int g = 0; g < GPT; ++g) {
+                            rv[g][c] = c < lim[g] ? rv[g][c] : 0xff800000u;   // -inf
+                            mx = fmaxf(mx, __uint_as_float(rv[g][c]));
+                        }
                     }
                 }
                 if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 2);
-                // combine the two column halves of the row (partner warp: same quadrant)
-                float* rd = red + (gt & 1) * 2 * BM;
+                // combine the column splits of the row (partner warps: same quadrant)
+                float* rd = red + (gt & 1) * NQ * BM;
                 rd[h * BM + r] = mx;
-                named_bar(1 + q4, 64);
-                mx = fmaxf(mx, rd[(h ^ 1) * BM + r]) * sc;
+                named_bar(1 + q4, 32 * NQ);
+#pragma unroll
+                for (int q = 1; q < NQ; ++q) mx = fmaxf(mx, rd[((h + q) % NQ) * BM + r]);
+                mx *= sc;
                 if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 3);
                 // lazy rescale: keep the stale max unless it grew by > kLazy (both
                 // threads of a row decide alike).  The O correction is warp-collective
@@ -623,13 +636,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mbar_wait(BAR(O_FULL + (sb ^ 1)), ((gt - 1) >> 1) & 1);   // PV(t-1) done
                     tc_fence_after();
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
+                    for (int c = 0; c < CPT / 16; ++c) {
                         uint32_t o[16];
-                        TA_TMEM_LD16(tmem + lane_addr + TMEM_O + h * 64 + c * 16, o);
+                        TA_TMEM_LD16(tmem + lane_addr + TMEM_O + h * CPT + c * 16, o);
                         tmem_wait_ld();
 #pragma unroll
                         for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
-                        TA_TMEM_ST16(tmem + lane_addr + TMEM_O + h * 64 + c * 16, o);
+                        TA_TMEM_ST16(tmem + lane_addr + TMEM_O + h * CPT + c * 16, o);
                     }
                 }
                 if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 5);
@@ -637,28 +650,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     // P = exp2(s * scale - m) -> bf16 pairs -> S columns [16g, 16g+8); l += sum(P)
                     const float negm = m == -INFINITY ? 0.f : -m;
                     float la = 0.f;
-                    auto emit = [&](const uint32_t (&rv)[16], int g) {
+                    // P past ng lands in S columns PV never reads
+#pragma unroll
+                    for (int g = 0; g < GPT; ++g) {
                         uint32_t pk[8];
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
-                            const float p0 = ex2(fmaf(__uint_as_float(rv[2 * c]), sc, negm));
-                            const float p1 = ex2(fmaf(__uint_as_float(rv[2 * c + 1]), sc, negm));
+                            const float p0 = ex2(fmaf(__uint_as_float(rv[g][2 * c]), sc, negm));
+                            const float p1 = ex2(fmaf(__uint_as_float(rv[g][2 * c + 1]), sc, negm));
                             la += p0 + p1;
                             pk[c] = pack_bf16(p0, p1);
                         }
                         TA_TMEM_ST8(s_addr + 16 * (g0 + g), pk);
-                    };
-                    // P past ng lands in S columns PV never reads
-                    emit(r0, 0);
-                    emit(r1, 1);
-                    emit(r2, 2);
-                    emit(r3, 3);
+                    }
                     l += la;
                 } else if (warp_live) {
                     // no row of this warp attends my half of the tile: P = 0
                     const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-                    for (int g = 0; g < 4; ++g)
+                    for (int g = 0; g < GPT; ++g)
                         if (g0 + g < ng) TA_TMEM_ST8(s_addr + 16 * (g0 + g), z);
                 }
                 tmem_wait_st();
@@ -672,7 +682,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (threadIdx.x == TRACE_TID) TA_MARK(a, 185, __float_as_uint(l));
                 if (has_next && t == I.tile_begin) {
                     // next item's Q -> the other Q buffer (free once item k-1's QK is done)
-                    uint4 qv[8];
+                    uint4 qv[QV];
                     q_fetch(item_at(k + 1), nleaf, qv);
                     if (k >= 1) mbar_wait(BAR(Q_FREE + ((k + 1) & 1)), ((k - 1) >> 1) & 1);
                     tc_fence_after();
@@ -686,8 +696,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc_fence_after();
             TA_TRACE_EPI(a, k, 1);
             redl[h * BM + r] = l;
-            named_bar(1 + q4, 64);
-            l += redl[(h ^ 1) * BM + r];
+            named_bar(1 + q4, 32 * NQ);
+#pragma unroll
+            for (int q = 1; q < NQ; ++q) l += redl[((h + q) % NQ) * BM + r];
             if (threadIdx.x == TRACE_TID) TA_MARK(a, 186, __float_as_uint(l));
             TA_TRACE_EPI(a, k, 4);
             const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -714,19 +725,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // fp32 rows go out in EPI_PASSES column passes through a staging
                 // row of 256 / EPI_PASSES bytes (the SMEM it saves deepens the V ring)
                 const int npass = st_bf16 ? 1 : EPI_PASSES;
-                const int cpp = 4 / npass;   // 16-column chunks per pass
+                const int cpp = (CPT / 16) / npass;   // 16-column chunks per pass
                 char* dst = nullptr;
                 if (code != kSlotUnused)
-                    dst = code >= 0 ? reinterpret_cast<char*>(a.part_o + ((size_t)code * G + g_in) * DH + 64 * h)
+                    dst = code >= 0 ? reinterpret_cast<char*>(a.part_o + ((size_t)code * G + g_in) * DH + CPT * h)
                                     : reinterpret_cast<char*>(a.out) +
-                                          (((size_t)(-1 - code) * a.hq_loc + I.head * G + g_in) * DH + 64 * h) * (a.out_bf16 ? 2 : 4);
+                                          (((size_t)(-1 - code) * a.hq_loc + I.head * G + g_in) * DH + CPT * h) * (a.out_bf16 ? 2 : 4);
 #pragma unroll 1
                 for (int pass = 0; pass < npass; ++pass) {
                     if (pass > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #pragma unroll 1
                     for (int c = pass * cpp; c < (pass + 1) * cpp; ++c) {
                         uint32_t o[16];
-                        TA_TMEM_LD16(tmem + lane_addr + TMEM_O + h * 64 + c * 16, o);
+                        TA_TMEM_LD16(tmem + lane_addr + TMEM_O + h * CPT + c * 16, o);
                         tmem_wait_ld();
                         float f[16];
 #pragma unroll
@@ -745,7 +756,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         }
                     }
                     if (dst) {
-                        const uint32_t nb = st_bf16 ? 128u : 256u / npass;
+                        const uint32_t nb = st_bf16 ? (uint32_t)(CPT * 2) : (uint32_t)(CPT * 4) / npass;
                         fence_proxy_async();   // the staging writes -> visible to the bulk copy
                         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + pass * nb), "r"(srow),
                                      "r"(nb)
