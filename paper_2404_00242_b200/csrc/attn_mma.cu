@@ -109,6 +109,9 @@ constexpr int TMEM_S = 0, TMEM_O = 256, TMEM_Q = 384;   // S0, S1 (P aliased), O
 constexpr float kLazy = 8.0f;                            // rescale O only when the max grows by > 2^8
 // A/B ablations and the light CTA-phase trace (scripts/build_variant.sh,
 // scripts/light_spans.py); never defined in the product build
+#ifndef TA_ABL_NOMMA
+#define TA_ABL_NOMMA 0    // issuers commit without issuing MMAs (timing only, with TA_ABL_STREAM)
+#endif
 #ifndef TA_ABL_STREAM
 #define TA_ABL_STREAM 0   // softmax warps release each tile without reading S (timing only)
 #endif
@@ -185,6 +188,16 @@ __device__ __forceinline__ long long gtimer() {
             }                                                                                      \
         }                                                                                          \
     } while (0)
+// per-item marks of the first 3 items (slots 198 + 8 * item + j): 0 QK
+// issuer past Q_FULL, 1 first QK committed, 2 epilogue saw O_FULL, 3 staging
+// free, 4 copies issued, 5 first PV committed, 6 softmax item setup done,
+// 7 softmax at the first tile's S wait
+#define TA_TRACE_ITEM(a, item, j)                                                                  \
+    do {                                                                                           \
+        if constexpr (TRACE) {                                                                     \
+            if ((a).trace && (item) < 3) (a).trace[blockIdx.x * TRACE_SLOTS + 198 + 8 * (item) + (j)] = clock64(); \
+        }                                                                                          \
+    } while (0)
 #define TA_TRACE(a, t, k)                                                                          \
     do {                                                                                           \
         if constexpr (TRACE) {                                                                     \
@@ -244,7 +257,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         a.trace[blockIdx.x * TRACE_SLOTS + 193] = clock64();
     }
     if (threadIdx.x == 0) TA_MARK(a, 180, blockIdx.x);
-    if (TA_LIGHT_TRACE && !TRACE && a.trace && threadIdx.x == 0) a.trace[blockIdx.x * TRACE_SLOTS] = gtimer();
+    if (TA_LIGHT_TRACE && !TRACE && a.trace && threadIdx.x == 0) {
+        a.trace[blockIdx.x * TRACE_SLOTS] = gtimer();
+        unsigned smid_;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));
+        a.trace[blockIdx.x * TRACE_SLOTS + 41] = smid_;
+    }
     ItemDesc* s_item = reinterpret_cast<ItemDesc*>(smem + SMEM_ITEM);
     TileDesc* s_td = reinterpret_cast<TileDesc*>(smem + SMEM_TD);
     TileMeta* s_tm = reinterpret_cast<TileMeta*>(smem + SMEM_TM);
@@ -367,7 +385,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // synchronous, or ta_kv_append, whose rows the host knows)
     const int n_early = a.early_kv ? s_hdr[blob::N_EARLY] : 0;
     if (!(warp == 0 && lane == 0)) pdl_wait();
-    if (threadIdx.x == 0) TA_LIGHT(40, s_hdr[1]);
+    if (threadIdx.x == 32) TA_LIGHT(40, s_hdr[1]);   // after the dependency wait (warp 1)
     if (TRACE && threadIdx.x == 0) timeline_mark(a.timeline, 0, true);
     if (TRACE && a.trace && threadIdx.x == 0) {
         a.trace[blockIdx.x * TRACE_SLOTS] = gtimer();
@@ -438,6 +456,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (gt == 0) TA_MARK(a, 183, bytes);
                     if (gt == 0) TA_LIGHT(2, bytes);
                     mbar_wait(BAR(EMPTYV + sv), phv ^ 1);
+                    TA_TRACE(a, gt, 4);
                     mbar_expect_tx(BAR(FULLV + sv), bytes);
                     std::memcpy(&boxes, td.box, 8);
 #pragma unroll 1
@@ -458,6 +477,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const ItemDesc I = item_at(k);
                 const int qb = k & 1;   // Q buffer of this item
                 mbar_wait(BAR(Q_FULL + qb), (k >> 1) & 1);
+                TA_TRACE_ITEM(a, k, 0);
                 for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
                     const int ng = td_at(gt, t).ng;
                     const int s = gt % NK, sb = gt & 1;
@@ -467,12 +487,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const uint32_t sK = sbase + SMEM_K + (uint32_t)s * TILE;
                     const uint32_t id = idesc_bf16(BM, 16 * ng, 0, 0);
 #pragma unroll
-                    for (int kq = 0; kq < DH / 16; ++kq) {
+                    for (int kq = 0; kq < (TA_ABL_NOMMA ? 0 : DH / 16); ++kq) {
                         const uint32_t off = (uint32_t)((kq >> 2) * HALF + (kq & 3) * 32);
                         mma_bf16_ts(tmem + TMEM_S + sb * 128, tmem + TMEM_Q + 64 * qb + 8 * kq, sdesc(sK + off, 16, 1024), id,
                                     kq > 0);
                     }
                     mma_commit(BAR(S_FULL + sb));
+                    if (t == I.tile_begin) TA_TRACE_ITEM(a, k, 1);
                     mma_commit(BAR(EMPTYK + s));
                 }
                 mma_commit(BAR(Q_FREE + qb));
@@ -495,10 +516,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const uint32_t id = idesc_bf16(BM, DH, 0, 1);
                     const bool first = t == I.tile_begin;
                     // P of group kk: bf16 pairs in columns [16kk, 16kk+8) of S buffer sb
-                    for (int kk = 0; kk < ng; ++kk)
+                    for (int kk = 0; kk < (TA_ABL_NOMMA ? 0 : ng); ++kk)
                         mma_bf16_ts(tmem + TMEM_O, tmem + TMEM_S + sb * 128 + 16 * kk, sdesc(sV + kk * 2048, HALF, 1024),
                                     id, (!first || kk > 0) ? 1u : 0u);
                     mma_commit(BAR(EMPTYV + s));
+                    if (first) TA_TRACE_ITEM(a, k, 5);
                     mma_commit(BAR(S_FREE + sb));
                     mma_commit(BAR(O_FULL + sb));
                 }
@@ -569,6 +591,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 nleaf = r < In.n_slots * G ? leaf_at(k + 1, In, r / G) : -1;
                 if (nleaf >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(q_row(In, nleaf)));
             }
+            if (threadIdx.x == TRACE_TID) TA_TRACE_ITEM(a, k, 6);
             for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
                 const TileDesc td = td_at(gt, t);
                 uint32_t info[GPT];
@@ -593,6 +616,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const bool warp_att = __any_sync(0xffffffffu, att);
                 const int sb = gt & 1;
                 const uint32_t s_addr = tmem + lane_addr + TMEM_S + sb * 128;
+                if (threadIdx.x == TRACE_TID && t == I.tile_begin) TA_TRACE_ITEM(a, k, 7);
                 mbar_wait(BAR(S_FULL + sb), (gt >> 1) & 1);
                 if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt, 1);
                 tc_fence_after();
@@ -693,6 +717,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // ---- epilogue
             mbar_wait(BAR(O_FULL + ((gt - 1) & 1)), ((gt - 1) >> 1) & 1);   // PV(last) and all before it
             TA_TRACE_EPI(a, k, 0);
+            if (threadIdx.x == TRACE_TID) TA_TRACE_ITEM(a, k, 2);
             tc_fence_after();
             TA_TRACE_EPI(a, k, 1);
             redl[h * BM + r] = l;
@@ -717,11 +742,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // background instead of stalling the softmax warps behind the
                 // saturated read stream.  Compact loops: this code runs once per
                 // item, I-cache cold.
+                {
                 const uint32_t srow = sbase + SMEM_EPI + (uint32_t)(((warp - SOFT0) * 32 + lane) * EPI_ROW);
                 const bool st_bf16 = code < 0 && a.out_bf16;
                 // the row's previous bulk copy (an earlier item) has read the staging
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 TA_TRACE_EPI(a, k, 3);
+                if (threadIdx.x == TRACE_TID) TA_TRACE_ITEM(a, k, 3);
                 // fp32 rows go out in EPI_PASSES column passes through a staging
                 // row of 256 / EPI_PASSES bytes (the SMEM it saves deepens the V ring)
                 const int npass = st_bf16 ? 1 : EPI_PASSES;
@@ -766,8 +793,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         if (threadIdx.x == TRACE_TID && k + 1 == n_items) TA_LIGHT(5, srow);
                     }
                 }
+                }
             }
             TA_TRACE_EPI(a, k, 2);
+            if (threadIdx.x == TRACE_TID) TA_TRACE_ITEM(a, k, 4);
             tc_fence_before();
             if (threadIdx.x == TRACE_TID) TA_TRACE(a, gt - 1, 7);
             if constexpr (TRACE) {

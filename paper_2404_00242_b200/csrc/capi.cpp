@@ -306,6 +306,9 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
         } else if (k == "tile_cost") {
             if (v < 0) fail(TA_ERR_INVALID_ARGUMENT, "tile_cost must be >= 0");
             c->opt.tile_cost = (int)v;
+        } else if (k == "box_cost") {
+            if (v < 0) fail(TA_ERR_INVALID_ARGUMENT, "box_cost must be >= 0");
+            c->opt.box_cost = (int)v;
         } else if (k == "row_cost") {
             if (v < 0) fail(TA_ERR_INVALID_ARGUMENT, "row_cost must be >= 0");
             c->opt.row_cost = (int)v;

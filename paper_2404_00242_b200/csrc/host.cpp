@@ -747,7 +747,8 @@ void build_schedule(const Tree& t, const PagePool& pool, const Plan& plan, int G
             const uint32_t info = S.grp_info[S.tiles[i].grp_begin + g];
             pairs += (int64_t)(info & 0xffu) * (int64_t)((info >> 20) - ((info >> 8) & 0xfffu)) * G;
         }
-        tcost[i] = 16LL * S.tiles[i].ng + opt.tile_cost + (int64_t)opt.row_cost * pairs / (128 * 128);
+        tcost[i] = 16LL * S.tiles[i].ng + opt.tile_cost + (int64_t)opt.box_cost * S.tiles[i].nbox +
+                   (int64_t)opt.row_cost * pairs / (128 * 128);
         tile_sum += tcost[i];
         S.kv_rows_loaded += 16LL * S.tiles[i].ng * n_heads;
     }

@@ -264,6 +264,7 @@ struct SchedOptions {
     int tile_groups = 8;       // groups per tile
     int num_ctas = 148;        // persistent grid
     int tile_cost = 24;        // fixed per-tile cost, in box rows
+    int box_cost = 0;          // per TMA box of a tile (partial tiles of scattered rows issue more), in box rows
     int row_cost = 15;         // softmax cost of a dense tile (128 x 128 attended pairs), in box rows
                                // (swept: 15 beats 60 by 3 % on few-shot, 14 % on 70B, ties on reasoning)
     int item_cost = 300;       // cost of starting an item (Q load, epilogue), in box rows

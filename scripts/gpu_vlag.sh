@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/vlag_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/vlag_pytest.log
+VARIANTS="base vlag0" CFGS="few_shot reasoning spec_t64 spec_t256 few_shot_70b_shard" bash scripts/gpu_ab.sh

@@ -25,7 +25,7 @@ __device__ __forceinline__ void tma2d(uint32_t dst, const void* map, int c0, int
 
 template <int H, int S>
 __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv,
-                                                       int tiles, int rows_total) {
+                                                       int tiles, int rows_total, int share, int seq) {
     extern __shared__ uint8_t raw[];
     uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
     uint64_t* bars = (uint64_t*)(sm + S * 65536);
@@ -43,8 +43,14 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
             mbar_expect(b0 + 8 * s, 65536);
             const uint32_t dst = smem_u32(sm + s * 65536);
             // pseudo-random tile base row (128-row aligned), distinct per CTA/tile
-            const long long tile_id = (long long)blockIdx.x * tiles + t;
-            const int row0 = (int)((tile_id * 2654435761LL) % (rows_total / 128)) * 128;
+            // share > 0: groups of `share` CTAs read the same tile sequence
+            // (share < 0: the same, each CTA of a group offset by one tile)
+            const int grp = share > 0 ? share : (share < 0 ? -share : 1);
+            const long long tile_id = share == 0 ? (long long)blockIdx.x * tiles + t
+                                                 : (long long)(blockIdx.x / grp) * tiles + (share > 0 ? t : (t + blockIdx.x % grp) % tiles);
+            // hashed tile positions, or (seq) contiguous tile runs
+            const int row0 = seq ? (int)((tile_id % (rows_total / 128)) * 128)
+                                 : (int)((tile_id * 2654435761LL) % (rows_total / 128)) * 128;
             for (int b = 0; b < 128 / H; ++b) {
                 tma2d(dst + b * H * 128, &mk, 0, row0 + b * H, b0 + 8 * s);
                 tma2d(dst + 16384 + b * H * 128, &mk, 64, row0 + b * H, b0 + 8 * s);
@@ -63,22 +69,22 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
 }
 
 template <int H, int S>
-float run(CUtensorMap& mk, CUtensorMap& mv, int ctas, int tiles, int rows) {
+float run(CUtensorMap& mk, CUtensorMap& mv, int ctas, int tiles, int rows, int share = 0, int seq = 0) {
     const int smem = S * 65536 + 2048;
     cudaFuncSetAttribute(stream_kernel<H, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    stream_kernel<H, S><<<ctas, 64, smem>>>(mk, mv, tiles, rows);
+    stream_kernel<H, S><<<ctas, 64, smem>>>(mk, mv, tiles, rows, share, seq);
     cudaEventRecord(a);
-    for (int i = 0; i < 5; ++i) stream_kernel<H, S><<<ctas, 64, smem>>>(mk, mv, tiles, rows);
+    for (int i = 0; i < 5; ++i) stream_kernel<H, S><<<ctas, 64, smem>>>(mk, mv, tiles, rows, share, seq);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
     cudaEventElapsedTime(&ms, a, b);
     const double bytes = 5.0 * ctas * tiles * 65536.0;
     const float gbs = (float)(bytes / (ms * 1e-3) / 1e9);
-    printf("H=%3d S=%d ctas=%4d tiles=%3d : %8.1f GB/s  (%s)\n", H, S, ctas, tiles, gbs, cudaGetErrorString(cudaGetLastError()));
+    printf("H=%3d S=%d ctas=%4d tiles=%3d share=%2d seq=%d : %8.1f GB/s  (%s)\n", H, S, ctas, tiles, share, seq, gbs, cudaGetErrorString(cudaGetLastError()));
     return gbs;
 }
 
@@ -111,5 +117,21 @@ int main() {
     run<16, 2>(k16, v16, 112, 16, rows);
     run<128, 2>(k128, v128, 112, 16, rows);
     run<16, 3>(k16, v16, 112, 16, rows);
+    // L2-resident working sets (a 16k-token prefix x 8 heads = 128k rows, 64 MB
+    // of K+V; and 32k rows, 16 MB): the ceiling for re-read tiles that hit L2
+    for (int small : {131072, 32768}) {
+        printf("L2-resident working set: %d rows (%.0f MB K+V)\n", small, small * 512.0 / 1e6);
+        run<128, 2>(k128, v128, 148, 64, small);
+        run<128, 3>(k128, v128, 148, 64, small);
+        run<16, 2>(k16, v16, 148, 64, small);
+    }
+    // tiles shared by groups of CTAs (the lanes of a wide stripe), 1 GB of
+    // rows (L2-resident only through the sharing)
+    printf("shared tile sequences (2 GiB tensors: a tile comes from DRAM once per group)\n");
+    for (int sh : {1, 2, 4, 8, -2, -4, -8}) run<128, 2>(k128, v128, 148, 64, rows, sh);
+    for (int sh : {8, -8}) run<128, 3>(k128, v128, 148, 64, rows, sh);
+    printf("contiguous tile runs\n");
+    for (int sh : {0, 2, 8, -8}) run<128, 2>(k128, v128, 148, 64, rows, sh, 1);
+    run<128, 2>(k128, v128, 148, 64, 131072, 0, 1);
     return 0;
 }
