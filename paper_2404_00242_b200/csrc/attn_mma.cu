@@ -62,7 +62,7 @@ constexpr int CPT = 128 / NQ;                            // S / O / Q columns pe
 constexpr int GPT = 8 / NQ;                              // 16-column S groups per softmax thread
 constexpr int NTHREADS = 96 + 128 * NQ;                  // 3 issuer warps + 4 * NQ softmax warps
 constexpr int NSOFT = 128 * NQ;                          // softmax threads
-static_assert(NQ == 2 || NQ == 4, "column splits");
+static_assert(NQ == 1 || NQ == 2 || NQ == 4, "column splits");
 constexpr int NK = TA_NK;                                // K ring depth (a K tile is released by its QK)
 constexpr int NV = TA_NV;                                // V ring depth (a V tile waits for the softmax and PV)
 constexpr int HALF = BM * 128;                           // one 64-column half of a [128][128] bf16 tile
@@ -595,7 +595,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
                 const TileDesc td = td_at(gt, t);
                 uint32_t info[GPT];
-                if constexpr (GPT == 4) {
+                if constexpr (GPT == 8) {
+                    const uint4* inf = reinterpret_cast<const uint4*>(tm_at(gt, t)->info);
+                    const uint4 i0 = inf[0], i1 = inf[1];
+                    info[0] = i0.x; info[1] = i0.y; info[2] = i0.z; info[3] = i0.w;
+                    info[4] = i1.x; info[5] = i1.y; info[6] = i1.z; info[7] = i1.w;
+                } else if constexpr (GPT == 4) {
                     const uint4 inf = *reinterpret_cast<const uint4*>(tm_at(gt, t)->info + 4 * h);
                     info[0] = inf.x; info[1] = inf.y; info[2] = inf.z; info[3] = inf.w;
                 } else {
@@ -641,7 +646,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // combine the column splits of the row (partner warps: same quadrant)
                 float* rd = red + (gt & 1) * NQ * BM;
                 rd[h * BM + r] = mx;
-                named_bar(1 + q4, 32 * NQ);
+                if constexpr (NQ > 1) named_bar(1 + q4, 32 * NQ);
 #pragma unroll
                 for (int q = 1; q < NQ; ++q) mx = fmaxf(mx, rd[((h + q) % NQ) * BM + r]);
                 mx *= sc;
@@ -721,7 +726,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc_fence_after();
             TA_TRACE_EPI(a, k, 1);
             redl[h * BM + r] = l;
-            named_bar(1 + q4, 32 * NQ);
+            if constexpr (NQ > 1) named_bar(1 + q4, 32 * NQ);
 #pragma unroll
             for (int q = 1; q < NQ; ++q) l += redl[((h + q) % NQ) * BM + r];
             if (threadIdx.x == TRACE_TID) TA_MARK(a, 186, __float_as_uint(l));
