@@ -41,6 +41,7 @@ struct ta_ctx {
     uint64_t fast_log_version = ~0ull;   // tree version after the last logged append
     bool fast_bad = true;
     int64_t n_fast_prepares = 0;
+    int64_t n_noop_prepares = 0;        // ta_prepare calls that found nothing to rebuild
 
     // TMA descriptors (CUtensorMap, 128 B) over the whole K / V pools
     alignas(64) unsigned char tmap_k[512];   // CUtensorMap for 16/32/64/128-row boxes
@@ -861,6 +862,14 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
         // one decode step = plan + schedule + metadata upload, reused by every layer
         const auto t0 = std::chrono::steady_clock::now();
+        // nothing changed since the last prepare (same tree version, block size
+        // and options; no appends logged): the device schedule stands
+        if (c->prepared && c->prepared_version == c->tree.version && c->prepared_bs == bs && c->fast_log.empty() &&
+            !c->early_kv) {
+            c->t_plan_ns = c->t_sched_ns = c->t_upload_ns = 0;
+            ++c->n_noop_prepares;
+            return;
+        }
         // decode-step fast path: only ta_tree_append_leaves since the last
         // prepare, and every new token extends its leaf's tail group -> patch the
         // schedule in place (the flatten plan is rebuilt on demand only).  Off
