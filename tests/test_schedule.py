@@ -230,8 +230,8 @@ def test_coverage_zero_token_and_holders():
 
 
 def test_coverage_item_cost_repartition():
-    """The re-partition with the higher item cost (CTAs with many items) and
-    both CTA partitions keep the coverage contract."""
+    """The re-partition with the higher item cost (CTAs with many items), the
+    per-box tile cost and both CTA partitions keep the coverage contract."""
     rng = core.Rng(404)
     for trial in range(6):
         ctx = _ctx(G=4, dtype="bf16", n_kv=2)
@@ -239,6 +239,7 @@ def test_coverage_item_cost_repartition():
         ctx.set_option("item_cost_many", (450, 5000)[trial % 2])
         ctx.set_option("num_ctas", (13, 148)[trial % 2])
         ctx.set_option("minmax", trial % 3 != 2)   # min-max budget / equal split points
+        ctx.set_option("box_cost", (0, 40, 0)[trial % 3])   # per-box term of the tile cost
         t = core.random_tree(rng, max_leaves=50, max_node_tokens=200)
         ctx.restore(*t.snapshot())
         check_coverage(ctx, t, 128)
