@@ -808,6 +808,11 @@ def main():
         return
 
     import torch
+    # TA_BENCH_SHARE_GPU=1 (testing the N > 1 code path on a box with fewer
+    # GPUs than ranks): ranks share devices round-robin and talk over gloo
+    share = os.environ.get("TA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     if args.replay:
         names = REPLAY_PRESETS if args.replay == "all" else args.replay.split(",")
@@ -815,7 +820,10 @@ def main():
         return
     if world > 1 or (args.prefix_split and "RANK" in os.environ):
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     with ClockSampler(local_rank) as clocks:
         head = measure(args.config, cfg, args, world, rank, local_rank, clocks=clocks, with_cpu=True)
