@@ -300,3 +300,14 @@ def test_repeat_launches_deterministic():
     for o in outs:
         assert torch.equal(o, outs[0])
     assert np.array_equal(outs[0].float().cpu().numpy().reshape(len(leaves), -1), out)
+    # a prepare with nothing changed keeps the device schedule (no host work)
+    ctx.prepare(128)
+    st = ctx.io_stats()
+    assert st.host_plan_ns == 0 and st.host_upload_ns == 0
+    again = ctx.attend(0, q)
+    torch.cuda.synchronize()
+    assert torch.equal(again, outs[0])
+    # ... and a real change is not skipped: a new leaf re-plans
+    ctx.branch(int(leaves[0]), [1])
+    ctx.prepare(128)
+    assert ctx.io_stats().host_plan_ns > 0
