@@ -322,6 +322,10 @@ def measure(name, cfg, args, world, rank, local_rank, clocks=None, with_cpu=Fals
         torch.cuda.synchronize()
 
     def step():
+        # a prepare of an unchanged tree is a no-op (ta_prepare keeps the
+        # schedule); the headline step re-plans and re-uploads every step, as
+        # after a tree change (any schedule option marks the context stale)
+        ctx.set_option("tile_groups", 8)
         ctx.prepare(128, stream)
         if graph is not None:
             graph.replay()
@@ -409,6 +413,7 @@ def measure(name, cfg, args, world, rank, local_rank, clocks=None, with_cpu=Fals
             # every layer's output is back in host memory
             for layer in range(L_layers):
                 ctx.attend_host_async(layer, qn[layer], on[layer], stream=stream)
+            ctx.set_option("tile_groups", 8)   # re-plan and re-upload, as in the device-timed step
             ctx.prepare(128, stream)
             ctx.attend_host_wait()
 
