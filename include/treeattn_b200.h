@@ -96,7 +96,7 @@ ta_status ta_ctx_create(int device, const ta_shape* shape, ta_ctx** out);
 ta_status ta_ctx_destroy(ta_ctx* ctx);
 /* tuning knobs: "use_mma", "fma_max_rows", "mma_max_rows", "tile_groups",
  * "tile_cost", "box_cost", "row_cost", "item_cost", "item_cost_many", "many_items",
- * "minmax", "num_ctas", "final_direct", "fused_merge", "pdl",
+ * "minmax", "num_ctas", "final_direct", "fused_merge", "pdl", "fuse_append",
  * "prefetch_tiles"; debug: "trace_ptr", "timeline_ptr" */
 ta_status ta_set_option(ta_ctx* ctx, const char* key, int64_t value);
 
@@ -147,7 +147,11 @@ ta_status ta_kv_write(ta_ctx* ctx, int layer, int32_t node, int64_t tok_begin, i
  * ta_prepare are uploaded by the next ta_prepare; ta_kv_append then writes
  * that layer's rows k, v [n_rows][n_local_kv_heads][d_head] (device, in
  * append order) with one kernel and no host synchronisation.  The row count
- * is read on the device, so the call can live in a captured CUDA graph. */
+ * is read on the device, so the call can live in a captured CUDA graph.
+ * With the tcgen05 kernel (bf16, d 128, fused merge) and option
+ * "fuse_append" (default 1) the call launches nothing: it records k / v, and
+ * the layer's next ta_attend writes each row from the CTA that loads it,
+ * right before its tile (k / v must stay valid until that ta_attend). */
 ta_status ta_kv_append(ta_ctx* ctx, int layer, const void* k, const void* v, void* stream);
 /* rows the last ta_prepare uploaded for ta_kv_append */
 int64_t ta_kv_append_rows(ta_ctx* ctx);

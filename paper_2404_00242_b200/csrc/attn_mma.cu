@@ -143,7 +143,7 @@ constexpr float kLazy = 8.0f;                            // rescale O only when 
 // issuer, and a waiter must never be two phases behind its barrier.
 enum { FULLK = 0, FULLV = NK, EMPTYK = NK + NV, EMPTYV = 2 * NK + NV, S_FULL = 2 * (NK + NV), S_FREE = S_FULL + 2,
        P_FULL = S_FULL + 4, O_FULL = S_FULL + 6, Q_FULL = S_FULL + 8, Q_FREE = S_FULL + 10, META_HEAD = S_FULL + 12,
-       META_TAIL = S_FULL + 13, NBAR = S_FULL + 14 };
+       META_TAIL = S_FULL + 13, APPEND = S_FULL + 14, NBAR = S_FULL + 15 };
 constexpr int TMEM_SLOT = 240;                           // offset of the TMEM address in the barrier block
 static_assert(NBAR * 8 <= TMEM_SLOT, "barriers overlap the TMEM slot");
 
@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         mbar_init(BAR(META_HEAD), 1);
         mbar_init(BAR(META_TAIL), 1);
+        mbar_init(BAR(APPEND), NSOFT);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
         // the schedule head: host-written before the launch, so read before the
@@ -429,11 +430,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // ===================== TMA producer =====================
         if (lane == 0) {
             int gt = 0;
+            // fused append: the first tile holding a row this launch writes
+            const int app_gt = a.app_k ? a.app_cta[blockIdx.x].z : INT_MAX;
             for (int k = 0; k < n_items; ++k) {
                 const ItemDesc I = item_at(k);
                 const int64_t row0 = a.layer_row0 + (int64_t)I.head * a.head_rows;
                 for (int t = I.tile_begin; t < I.tile_end; ++t, ++gt) {
                     if (gt == n_early) pdl_wait();
+                    if (gt == app_gt) mbar_wait(BAR(APPEND), 0);   // the softmax warps wrote the rows
                     const TileDesc td = td_at(gt, t);
                     const TileMeta* tmp = tm_at(gt, t);
                     const int s = gt % NK, sv = gt % NV;
@@ -566,6 +570,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_arrive(BAR(Q_FULL + qb));
         };
 
+        if (a.app_k) {
+            // fused ta_kv_append: this CTA's share of the step's new K / V rows
+            // into this layer's pools (a warp per row: lanes 0-15 K, 16-31 V),
+            // visible to the TMA loads the producer issues after the barrier
+            const int4 ce = a.app_cta[blockIdx.x];
+            const int n_loc = a.hq_loc / G;
+            for (int e = ce.x + (warp - SOFT0); e < ce.y; e += NSOFT / 32) {
+                const int4 en = a.app_list[e];
+                const bool is_v = lane >= 16;
+                const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(is_v ? a.app_v : a.app_k) +
+                                                                  ((size_t)en.x * n_loc + en.y) * DH);
+                uint4* dst = reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(is_v ? a.v : a.k)) +
+                                                      ((size_t)en.y * a.head_rows + en.z) * DH);
+                dst[lane & 15] = src[lane & 15];
+            }
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            mbar_arrive(BAR(APPEND));
+        }
         if (n_items > 0) {
             const ItemDesc I0 = item_at(0);
             uint4 qv[QV];

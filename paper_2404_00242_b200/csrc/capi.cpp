@@ -69,6 +69,10 @@ struct ta_ctx {
     int64_t t_plan_ns = 0, t_sched_ns = 0, t_upload_ns = 0;   // host time of the last ta_prepare
     std::vector<int32_t> pending_rows;   // pool rows of tokens appended since the last ta_prepare
     std::vector<int32_t> pending_sorted; // (sorted copy for the schedule blobs)
+    bool fuse_append = true;             // option "fuse_append": ta_kv_append deferred into ta_attend (tcgen05 path)
+    std::vector<const void*> app_k, app_v;   // per layer: new rows recorded by ta_kv_append for the next ta_attend
+    const int32_t* d_app_cta = nullptr;
+    const int32_t* d_app_list = nullptr;
     bool early_kv = false;               // option "early_kv": leading KV tiles loaded before the dependency wait
                                          // (off: in the 32-layer graph it measured +0.9 µs per few-shot layer,
                                          // the early loads competing with the previous launch's merge phase)
@@ -258,6 +262,8 @@ ta_status ta_ctx_create(int device, const ta_shape* s, ta_ctx** out) {
             c->head_stride = sh.max_pages * sh.page_tokens * (int64_t)sh.d_head;
             c->layer_elems = c->head_stride * sh.n_local_kv_heads;
             const size_t bytes = (size_t)c->layer_elems * sh.n_layers * c->esize;
+            c->app_k.assign(sh.n_layers, nullptr);
+            c->app_v.assign(sh.n_layers, nullptr);
             cuda_check(cudaMalloc(&c->kv_k, bytes), "cudaMalloc(K pool)");
             cuda_check(cudaMalloc(&c->kv_v, bytes), "cudaMalloc(V pool)");
             // Zeroed once: the tcgen05 kernel loads whole 16-row boxes, so the
@@ -338,6 +344,8 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->timeline = v;
         } else if (k == "trace_ptr") {
             c->trace = v;
+        } else if (k == "fuse_append") {
+            c->fuse_append = v != 0;
         } else if (k == "early_kv") {
             c->early_kv = v != 0;
         } else if (k == "fused_merge") {
@@ -461,6 +469,11 @@ int64_t ta_graph_epoch(ta_ctx* c) { return c ? c->graph_epoch : -1; }
 
 int64_t ta_fast_prepares(ta_ctx* c) { return c ? c->n_fast_prepares : -1; }
 
+// ta_kv_append is fused into ta_attend: tcgen05 schedules with the fused merge
+static bool fused_append(const ta_ctx* c) {
+    return c->fuse_append && c->sched.fused_merge && (int)c->app_k.size() == c->shape.n_layers;
+}
+
 ta_status ta_kv_append(ta_ctx* c, int layer, const void* k, const void* v, void* stream) {
     return guard([&] {
         need_device(c);
@@ -468,6 +481,13 @@ ta_status ta_kv_append(ta_ctx* c, int layer, const void* k, const void* v, void*
         if (layer < 0 || layer >= c->shape.n_layers) fail(TA_ERR_INVALID_ARGUMENT, "kv_append: layer out of range");
         if (!k || !v) fail(TA_ERR_INVALID_ARGUMENT, "kv_append: null key/value");
         if (((uintptr_t)k | (uintptr_t)v) & 15) fail(TA_ERR_INVALID_ARGUMENT, "kv_append: rows must be 16-byte aligned");
+        if (fused_append(c)) {
+            // written by the layer's next ta_attend, each row by the CTA that
+            // loads it, right before its tile: no launch of its own
+            c->app_k[layer] = k;
+            c->app_v[layer] = v;
+            return;
+        }
         cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
         char* dk = (char*)c->kv_k + (size_t)layer * c->layer_elems * c->esize;
         char* dv = (char*)c->kv_v + (size_t)layer * c->layer_elems * c->esize;
@@ -738,7 +758,7 @@ int fma_rows(int rows) { return rows <= 4 ? 4 : rows <= 8 ? 8 : 16; }
 // step never waits for the current step's upload.
 enum {
     P_HDR, P_TILES, P_TMETA, P_GROW, P_GINFO, P_ITEMS, P_CTAB, P_SLEAF, P_SOUT, P_MREC, P_PMERGE, P_PUBB, P_PUB,
-    P_EMPTY, P_OWNB, P_OWN, P_APPEND, P_HEADS, P_TAILS, NPART
+    P_EMPTY, P_OWNB, P_OWN, P_APPEND, P_HEADS, P_TAILS, P_APPC, P_APPL, NPART
 };
 
 static void upload_schedule(ta_ctx* c, cudaStream_t s) {
@@ -768,6 +788,8 @@ static void upload_schedule(ta_ctx* c, cudaStream_t s) {
         {c->pending_rows.data(), c->pending_rows.size() * 4},
         {S.cta_heads.data(), S.cta_heads.size()},
         {S.cta_tails.data(), S.cta_tails.size()},
+        {S.app_cta.data(), S.app_cta.size() * 4},
+        {S.app_list.data(), S.app_list.size() * 4},
     };
     static_assert(sizeof(src) / sizeof(src[0]) == NPART, "parts");
     // capacities (bytes): grow all exceeded parts by 1.5x, keep the rest
@@ -848,6 +870,8 @@ static void upload_schedule(ta_ctx* c, cudaStream_t s) {
     c->d_append_rows = (const int32_t*)at(P_APPEND);
     c->d_cta_heads = (const uint8_t*)at(P_HEADS);
     c->d_cta_tails = (const uint8_t*)at(P_TAILS);
+    c->d_app_cta = (const int32_t*)at(P_APPC);
+    c->d_app_list = (const int32_t*)at(P_APPL);
     c->n_append = (int64_t)c->pending_rows.size();
     c->pending_rows.clear();
     // The fused-merge counters are self-resetting; zero them only after a
@@ -865,7 +889,7 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         // nothing changed since the last prepare (same tree version, block size
         // and options; no appends logged): the device schedule stands
         if (c->prepared && c->prepared_version == c->tree.version && c->prepared_bs == bs && c->fast_log.empty() &&
-            !c->early_kv) {
+            !c->early_kv && c->n_append == 0) {
             c->t_plan_ns = c->t_sched_ns = c->t_upload_ns = 0;
             ++c->n_noop_prepares;
             return;
@@ -877,6 +901,11 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
         if (c->prepared && !c->fast_bad && !c->fast_log.empty() && c->tree.version == c->fast_log_version &&
             c->prepared_bs == bs && c->strategy == TA_STRATEGY_FLATTEN && c->sched.fused_merge && !c->early_kv &&
             patch_schedule_appends(c->sched, c->pool, c->fast_log)) {
+            if (c->fuse_append) {
+                std::vector<int32_t> tg(c->fast_log.size());
+                for (size_t i = 0; i < tg.size(); ++i) tg[i] = c->sched.tail_grp[c->fast_log[i].first];
+                build_append_lists(c->sched, c->shape.n_local_kv_heads, c->pending_rows, tg);
+            }
             const auto t2f = std::chrono::steady_clock::now();
             c->plan_valid = false;
             upload_schedule(c, (cudaStream_t)stream);
@@ -908,6 +937,8 @@ ta_status ta_prepare(ta_ctx* c, int bs, void* stream) {
             std::sort(c->pending_sorted.begin(), c->pending_sorted.end());
             build_cta_blobs(c->sched, c->pending_sorted);
             if (c->sched.fused_merge) build_tail_map(c->tree, c->pool, c->sched);
+            if (c->sched.fused_merge && c->fuse_append)
+                build_append_lists(c->sched, c->shape.n_local_kv_heads, c->pending_rows, {});
         }
         const auto t2 = std::chrono::steady_clock::now();
         upload_schedule(c, (cudaStream_t)stream);
@@ -969,6 +1000,13 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.timeline = reinterpret_cast<unsigned long long*>(c->timeline);
     a.prefetch_tiles = c->prefetch_tiles;
     a.early_kv = c->early_kv ? 1 : 0;
+    if (fused_append(c) && c->app_k[layer]) {
+        a.app_k = c->app_k[layer];
+        a.app_v = c->app_v[layer];
+        a.app_cta = (const int4*)c->d_app_cta;
+        a.app_list = (const int4*)c->d_app_list;
+        c->app_k[layer] = c->app_v[layer] = nullptr;   // one append per step and layer
+    }
 
     const SchedOptions o = effective_opts(c);
     // both kernels move q / out / lse rows in 16-byte units

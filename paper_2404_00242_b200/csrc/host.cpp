@@ -1248,4 +1248,69 @@ bool patch_schedule_appends(Schedule& S, const PagePool& pool,
     return true;
 }
 
+void build_append_lists(Schedule& S, int n_heads, const std::vector<int32_t>& pending_rows,
+                        const std::vector<int32_t>& tail_groups) {
+    const int n_cta = (int)S.cta_begin.size() - 1;
+    const int n_tiles = (int)S.tiles.size();
+    if ((int64_t)S.tile_loc.size() != (int64_t)n_heads * n_tiles) {
+        S.tile_loc.assign((size_t)n_heads * n_tiles, -1);
+        for (int c = 0; c < n_cta; ++c) {
+            int gt = 0;
+            for (int i = S.cta_begin[c]; i < S.cta_begin[c + 1]; ++i) {
+                const ItemDesc& it = S.items[i];
+                for (int t = it.tile_begin; t < it.tile_end; ++t, ++gt)
+                    S.tile_loc[(size_t)it.head * n_tiles + t] = (c << 16) | std::min(gt, 0xffff);
+            }
+        }
+    }
+    S.app_cta.assign((size_t)4 * n_cta, 0);
+    S.app_list.clear();
+    if (pending_rows.empty() || n_cta == 0) return;
+    // (append index, tile) for every group holding a pending row
+    std::vector<std::pair<int32_t, int32_t>> hits;
+    const bool known = tail_groups.size() == pending_rows.size();
+    if (known) {
+        for (size_t i = 0; i < pending_rows.size(); ++i)
+            if (tail_groups[i] >= 0) hits.push_back({(int32_t)i, S.grp_tile[tail_groups[i]]});
+    } else {
+        std::vector<std::pair<int32_t, int32_t>> sorted;   // (row, append index)
+        sorted.reserve(pending_rows.size());
+        for (size_t i = 0; i < pending_rows.size(); ++i) sorted.push_back({pending_rows[i], (int32_t)i});
+        std::sort(sorted.begin(), sorted.end());
+        for (int t = 0; t < n_tiles; ++t)
+            for (int g = S.tiles[t].grp_begin; g < S.tiles[t].grp_begin + S.tiles[t].ng; ++g) {
+                const int32_t r0 = S.grp_row[g], r1 = r0 + (int32_t)(S.grp_info[g] & 0xffu);
+                for (auto it = std::lower_bound(sorted.begin(), sorted.end(), std::make_pair(r0, INT32_MIN));
+                     it != sorted.end() && it->first < r1; ++it)
+                    hits.push_back({it->second, t});
+            }
+    }
+    // per CTA (counting sort): {append index, head, pool row}
+    std::vector<int32_t> n_per(n_cta + 1, 0);
+    for (const auto& [i, t] : hits)
+        for (int h = 0; h < n_heads; ++h) {
+            const int32_t loc = S.tile_loc[(size_t)h * n_tiles + t];
+            if (loc >= 0) ++n_per[(loc >> 16) + 1];
+        }
+    for (int c = 0; c < n_cta; ++c) n_per[c + 1] += n_per[c];
+    S.app_list.assign((size_t)4 * n_per[n_cta], 0);
+    std::vector<int32_t> fill(n_per.begin(), n_per.end() - 1);
+    for (int c = 0; c < n_cta; ++c) {
+        S.app_cta[4 * c] = n_per[c];
+        S.app_cta[4 * c + 1] = n_per[c + 1];
+        S.app_cta[4 * c + 2] = INT32_MAX;
+    }
+    for (const auto& [i, t] : hits)
+        for (int h = 0; h < n_heads; ++h) {
+            const int32_t loc = S.tile_loc[(size_t)h * n_tiles + t];
+            if (loc < 0) continue;
+            const int c = loc >> 16, gt = loc & 0xffff;
+            int32_t* e = &S.app_list[(size_t)4 * fill[c]++];
+            e[0] = i;
+            e[1] = h;
+            e[2] = pending_rows[i];
+            S.app_cta[4 * c + 2] = std::min(S.app_cta[4 * c + 2], gt);
+        }
+}
+
 }  // namespace ta

@@ -234,6 +234,14 @@ struct Schedule {
     std::vector<int32_t> grp_tile;
     std::vector<int32_t> tile_copy_begin;
     std::vector<uint32_t> tile_copy;
+    // fused decode-step append (tcgen05 kernel): (local head, tile) -> the CTA
+    // running it and its CTA-local tile index (cta << 16 | gt; -1: none), and
+    // per step the rows each CTA writes before loading them (ta_kv_append
+    // deferred into ta_attend): per CTA {begin, end, first local tile, 0} into
+    // app_list {append index, local head, pool row, 0}
+    std::vector<int32_t> tile_loc;
+    std::vector<int32_t> app_cta;     // int4 per CTA
+    std::vector<int32_t> app_list;    // int4 per entry
     std::vector<uint8_t> cta_heads;   // [n_ctas][blob::HEAD_BYTES]
     std::vector<uint8_t> cta_tails;   // packed tails (16-byte sections)
     std::vector<int32_t> empty;       // [n][2] (leaf, local head) pairs with no path tokens
@@ -254,6 +262,7 @@ struct Schedule {
         cta_pub_begin.clear(); cta_pub.clear(); cta_own_begin.clear(); cta_own.clear();
         cta_heads.clear(); cta_tails.clear();
         tail_grp.clear(); grp_tile.clear(); tile_copy_begin.clear(); tile_copy.clear();
+        tile_loc.clear(); app_cta.clear(); app_list.clear();
         n_lanes = n_partials = n_leaves = max_lane_rows = 0;
         kv_tokens_unique = kv_rows_loaded = masked_q_tokens = n_stripes = 0;
     }
@@ -297,5 +306,10 @@ bool patch_schedule_appends(Schedule& S, const PagePool& pool,
 // pending_rows: pool rows the step's ta_kv_append writes (sorted); a CTA's
 // leading tiles without any of them may be loaded before the dependency wait
 void build_cta_blobs(Schedule& S, const std::vector<int32_t>& pending_rows);
+// the fused append's per-CTA row lists for the rows appended since the last
+// prepare (pending_rows, in append order); tail_groups[i] >= 0: the group of
+// pending row i is known (fast path), else found by a scan of the groups
+void build_append_lists(Schedule& S, int n_heads, const std::vector<int32_t>& pending_rows,
+                        const std::vector<int32_t>& tail_groups);
 
 }  // namespace ta

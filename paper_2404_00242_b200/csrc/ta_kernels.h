@@ -72,6 +72,13 @@ struct AttnArgs {
     int out_bf16;
     long long* trace;         // optional clock64 trace (debug builds of the launch: a separate instantiation)
     int prefetch_tiles;       // first tiles of each CTA prefetched into L2 before the dependency wait
+    // tcgen05 kernel, fused decode-step append (ta_kv_append deferred into
+    // this launch): the step's new rows [n][n_loc][D] (nullptr: none) and
+    // per CTA the rows it writes into this layer's pools before loading them
+    const void* app_k;
+    const void* app_v;
+    const int4* app_cta;      // [n_ctas] {begin, end, first CTA-local tile, 0}
+    const int4* app_list;     // {append index, local head, pool row, 0}
     int early_kv;             // tcgen05 kernel: the CTA's leading tiles that no pending ta_kv_append row
                               // touches (blob header) are loaded before the dependency wait
     unsigned long long* timeline;   // debug: [4] = attn first start, attn last end, merge first start, merge last end (ns)
