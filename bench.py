@@ -563,6 +563,9 @@ def measure_decode_loop(name, cfg, args, world, rank, local_rank):
     host.clear()
     prep.clear()
     fast0 = ctx.fast_prepares()
+    # tcgen05 path (bf16, d 128) with the fused merge: ta_kv_append is fused into ta_attend
+    fused_append = (cfg["dtype"] == "bf16" and d == 128 and
+                    not any(o in args.opt for o in ("fuse_append=0", "fused_merge=0", "use_mma=0")))
     rec0 = state["recaptures"]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -580,12 +583,14 @@ def measure_decode_loop(name, cfg, args, world, rank, local_rank):
                                "upload": io.host_upload_ns / 1e3,
                                "total": (io.host_plan_ns + io.host_schedule_ns + io.host_upload_ns) / 1e3},
            "iterations": [it0 + W + 1, it0 + W + K], "graph_recaptures_in_timed_steps": state["recaptures"] - rec0,
-           "kv_append_rows_per_step": ctx.kv_append_rows(), "gpu_launches_per_step": L_layers * (1 + ctx.launches_per_attend()),
+           "kv_append_rows_per_step": ctx.kv_append_rows(),
+           # ta_kv_append launches a kernel only where it is not fused into ta_attend (tcgen05 + fused merge)
+           "gpu_launches_per_step": L_layers * (ctx.launches_per_attend() + (0 if fused_append else 1)),
            "fast_prepares_in_timed_steps": ctx.fast_prepares() - fast0,
            "host_prepare_us_per_step_incl_backpressure": {"median": statistics.median(prep) * 1e6, "max": max(prep) * 1e6},
            "kv_bytes_per_layer_at_end": io.kv_bytes,
            "path": "per step: ta_tree_append_leaves (1 token per leaf) + ta_prepare, then one graph replay of "
-                   "n_layers x (ta_kv_append + ta_attend)"}
+                   "n_layers x (ta_kv_append + ta_attend; the append fused into the attention launch on the tcgen05 path)"}
     del state, ctx
     torch.cuda.empty_cache()
     return res
