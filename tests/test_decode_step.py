@@ -64,8 +64,8 @@ def _content_row(node, t, dim, seed):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("use_graph,early_kv", [(False, 0), (True, 0), (True, 1)])
-def test_decode_loop_matches_oracle(use_graph, early_kv):
+@pytest.mark.parametrize("use_graph,early_kv,fuse_append", [(False, 0, 1), (True, 0, 1), (True, 1, 1), (True, 0, 0)])
+def test_decode_loop_matches_oracle(use_graph, early_kv, fuse_append):
     """40 decode steps of a few-shot tree (2 layers, GQA 8/2, bf16): each step
     appends one token per leaf, writes the new rows with ta_kv_append, re-plans
     and attends; outputs match the fp64 oracle on the final tree.  With
@@ -73,7 +73,9 @@ def test_decode_loop_matches_oracle(use_graph, early_kv):
     replayed after every re-plan (re-captured only if graph_epoch changes).
     early_kv: CTAs load their leading KV tiles before the dependency wait,
     except tiles holding rows of the step's ta_kv_append (the last step's
-    outputs depend on its appended rows)."""
+    outputs depend on its appended rows).  fuse_append: the new rows are
+    written inside the attention launch (default) or by ta_kv_append's own
+    kernel."""
     import torch
     from gpu_helpers import dense_reference, q_tensor
     prefix, nb, steps, d, hq, hkv, n_layers = 700, 9, 40, 128, 8, 2, 2
@@ -83,6 +85,7 @@ def test_decode_loop_matches_oracle(use_graph, early_kv):
     ctx = TreeAttention(n_layers=n_layers, n_q_heads=hq, n_kv_heads=hkv, d_head=d, kv_dtype="bf16",
                         max_pages=prefix // 16 + nb * (steps // 16 + 2) + 8)
     ctx.set_option("early_kv", early_kv)
+    ctx.set_option("fuse_append", fuse_append)
     ctx.restore(*t.snapshot())
     for layer in range(n_layers):
         k, v = core.node_kv(0, prefix, dim, seeds[layer])
