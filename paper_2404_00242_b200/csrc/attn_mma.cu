@@ -588,6 +588,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             asm volatile("fence.proxy.async.global;" ::: "memory");
             mbar_arrive(BAR(APPEND));
         }
+        if (a.q_flag) {
+            // host-buffer attend: q's copy-in (another stream) has landed
+            while ((int)(ld_acquire(a.q_flag) - a.q_seq) < 0) __nanosleep(64);
+        }
         if (n_items > 0) {
             const ItemDesc I0 = item_at(0);
             uint4 qv[QV];

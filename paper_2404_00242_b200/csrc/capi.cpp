@@ -129,6 +129,14 @@ struct ta_ctx {
     };
     IoSlot io_slot[kIoSlots];
     int io_next = 0;
+    // q-ready flags of the io slots (device words written by stream memory
+    // operations after each copy-in; the tcgen05 kernel polls its slot's
+    // flag instead of the compute stream waiting on an event, which would
+    // cut the launch chain between consecutive layers)
+    unsigned* io_flags = nullptr;
+    unsigned io_seq[kIoSlots] = {0, 0, 0};
+    const unsigned* q_flag = nullptr;   // set for the duration of one attend_impl
+    unsigned q_seq = 0;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
 
     ~ta_ctx() {
@@ -144,6 +152,7 @@ struct ta_ctx {
             cudaFree(stage_dev);
             cudaFreeHost(stage_host);
             cudaFree(io_dev);
+            cudaFree(io_flags);
             for (IoSlot& sl : io_slot) {
                 cudaFree(sl.dev);
                 if (sl.h2d) cudaEventDestroy(sl.h2d);
@@ -1000,6 +1009,8 @@ static void attend_impl(ta_ctx* c, int layer, const void* q, void* out, float* l
     a.timeline = reinterpret_cast<unsigned long long*>(c->timeline);
     a.prefetch_tiles = c->prefetch_tiles;
     a.early_kv = c->early_kv ? 1 : 0;
+    a.q_flag = c->q_flag;
+    a.q_seq = c->q_seq;
     if (fused_append(c) && c->app_k[layer]) {
         a.app_k = c->app_k[layer];
         a.app_v = c->app_v[layer];
@@ -1047,6 +1058,21 @@ ta_status ta_attend_host(ta_ctx* c, int layer, const void* q_host, void* out_hos
     });
 }
 
+// cuStreamWriteValue32 (driver API, reached through the runtime's entry-point
+// query so the library links only cudart); nullptr when unavailable
+typedef int (*WriteValue32Fn)(void* stream, unsigned long long addr, unsigned value, unsigned flags);
+static WriteValue32Fn write_value32() {
+    static WriteValue32Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (WriteValue32Fn) nullptr;
+        return (WriteValue32Fn)p;
+    }();
+    return fn;
+}
+
 ta_status ta_attend_host_async(ta_ctx* c, int layer, const void* q_host, void* out_host, void* stream) {
     return guard([&] {
         need_device(c);
@@ -1080,9 +1106,26 @@ ta_status ta_attend_host_async(ta_ctx* c, int layer, const void* q_host, void* o
         // the slot's previous use (its copy-out, hence its attention) is complete
         if (sl.used) cuda_check(cudaStreamWaitEvent(c->h2d_stream, sl.d2h, 0), "cudaStreamWaitEvent");
         cuda_check(cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, c->h2d_stream), "H2D q");
-        cuda_check(cudaEventRecord(sl.h2d, c->h2d_stream), "cudaEventRecord");
-        cuda_check(cudaStreamWaitEvent(s, sl.h2d, 0), "cudaStreamWaitEvent");
+        const int si = (int)(&sl - c->io_slot);
+        const bool poll = effective_opts(c).use_mma && write_value32() != nullptr;
+        if (poll) {
+            // the kernel waits for q on the device: no cross-stream dependency
+            // on the compute stream, so consecutive layers stay chained
+            if (!c->io_flags) {
+                cuda_check(cudaMalloc(&c->io_flags, 256), "cudaMalloc(io flags)");
+                cuda_check(cudaMemset(c->io_flags, 0, 256), "cudaMemset(io flags)");
+            }
+            const unsigned seq = ++c->io_seq[si];
+            if (write_value32()(c->h2d_stream, (unsigned long long)(uintptr_t)(c->io_flags + si), seq, 0) != 0)
+                fail(TA_ERR_CUDA, "cuStreamWriteValue32 failed");
+            c->q_flag = c->io_flags + si;
+            c->q_seq = seq;
+        } else {
+            cuda_check(cudaEventRecord(sl.h2d, c->h2d_stream), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(s, sl.h2d, 0), "cudaStreamWaitEvent");
+        }
         attend_impl(c, layer, dq, dout, nullptr, s);
+        c->q_flag = nullptr;
         cuda_check(cudaEventRecord(sl.kern, s), "cudaEventRecord");
         cuda_check(cudaStreamWaitEvent(c->d2h_stream, sl.kern, 0), "cudaStreamWaitEvent");
         cuda_check(cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, c->d2h_stream), "D2H out");

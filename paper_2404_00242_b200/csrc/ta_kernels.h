@@ -75,6 +75,11 @@ struct AttnArgs {
     // tcgen05 kernel, fused decode-step append (ta_kv_append deferred into
     // this launch): the step's new rows [n][n_loc][D] (nullptr: none) and
     // per CTA the rows it writes into this layer's pools before loading them
+    // tcgen05 kernel, host-buffer attend: q lands by an asynchronous copy on
+    // another stream, announced by a stream write of q_seq to *q_flag (nullptr:
+    // q is ready when the launch starts)
+    const unsigned* q_flag;
+    unsigned q_seq;
     const void* app_k;
     const void* app_v;
     const int4* app_cta;      // [n_ctas] {begin, end, first CTA-local tile, 0}
