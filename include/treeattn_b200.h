@@ -96,7 +96,7 @@ ta_status ta_ctx_create(int device, const ta_shape* shape, ta_ctx** out);
 ta_status ta_ctx_destroy(ta_ctx* ctx);
 /* tuning knobs: "use_mma", "fma_max_rows", "mma_max_rows", "tile_groups",
  * "tile_cost", "box_cost", "row_cost", "item_cost", "item_cost_many", "many_items",
- * "minmax", "num_ctas", "final_direct", "fused_merge", "pdl", "fuse_append",
+ * "minmax", "num_ctas", "final_direct", "fused_merge", "pdl", "fuse_append", "host_q_poll",
  * "prefetch_tiles"; debug: "trace_ptr", "timeline_ptr" */
 ta_status ta_set_option(ta_ctx* ctx, const char* key, int64_t value);
 

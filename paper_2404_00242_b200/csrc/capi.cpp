@@ -69,6 +69,7 @@ struct ta_ctx {
     int64_t t_plan_ns = 0, t_sched_ns = 0, t_upload_ns = 0;   // host time of the last ta_prepare
     std::vector<int32_t> pending_rows;   // pool rows of tokens appended since the last ta_prepare
     std::vector<int32_t> pending_sorted; // (sorted copy for the schedule blobs)
+    bool host_q_poll = true;             // option "host_q_poll": attend_host_async's kernel waits for q on the device
     bool fuse_append = true;             // option "fuse_append": ta_kv_append deferred into ta_attend (tcgen05 path)
     std::vector<const void*> app_k, app_v;   // per layer: new rows recorded by ta_kv_append for the next ta_attend
     const int32_t* d_app_cta = nullptr;
@@ -353,6 +354,8 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             c->timeline = v;
         } else if (k == "trace_ptr") {
             c->trace = v;
+        } else if (k == "host_q_poll") {
+            c->host_q_poll = v != 0;
         } else if (k == "fuse_append") {
             c->fuse_append = v != 0;
         } else if (k == "early_kv") {
@@ -368,7 +371,8 @@ ta_status ta_set_option(ta_ctx* c, const char* key, int64_t v) {
             fail(TA_ERR_INVALID_ARGUMENT, "unknown option " + k);
         }
         // launch-only knobs keep the prepared schedule
-        if (k != "trace_ptr" && k != "timeline_ptr" && k != "pdl" && k != "prefetch_tiles" && k != "early_kv")
+        if (k != "trace_ptr" && k != "timeline_ptr" && k != "pdl" && k != "prefetch_tiles" && k != "early_kv" &&
+            k != "host_q_poll")
             c->prepared = false;
     });
 }
@@ -1107,7 +1111,7 @@ ta_status ta_attend_host_async(ta_ctx* c, int layer, const void* q_host, void* o
         if (sl.used) cuda_check(cudaStreamWaitEvent(c->h2d_stream, sl.d2h, 0), "cudaStreamWaitEvent");
         cuda_check(cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, c->h2d_stream), "H2D q");
         const int si = (int)(&sl - c->io_slot);
-        const bool poll = effective_opts(c).use_mma && write_value32() != nullptr;
+        const bool poll = c->host_q_poll && effective_opts(c).use_mma && write_value32() != nullptr;
         if (poll) {
             // the kernel waits for q on the device: no cross-stream dependency
             // on the compute stream, so consecutive layers stay chained
