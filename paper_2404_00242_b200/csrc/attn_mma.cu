@@ -590,7 +590,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         if (a.q_flag) {
             // host-buffer attend: q's copy-in (another stream) has landed
-            while ((int)(ld_acquire(a.q_flag) - a.q_seq) < 0) __nanosleep(64);
+            // (a lost copy must fail loudly, not hang the GPU: trap after ~4 s)
+            const long long t0 = clock64();
+            while ((int)(ld_acquire(a.q_flag) - a.q_seq) < 0) {
+                __nanosleep(64);
+                if (clock64() - t0 > 8000000000LL) __trap();
+            }
         }
         if (n_items > 0) {
             const ItemDesc I0 = item_at(0);
